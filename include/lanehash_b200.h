@@ -1,0 +1,112 @@
+/*
+ * lanehash_b200.h — C ABI of the B200-native batched keyed-hash engine.
+ *
+ * The drop-in boundary for the reference package `lanehash`'s hash path
+ * (/root/reference/pkg, S = pkg/src/lanehash, T = pkg/tests).  Each entry
+ * point replaces one reference interface, cited beside it.  Plain pointers
+ * and sizes only: every `d_*` pointer is CUDA device memory owned by the
+ * caller, `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream) on the caller's current device.  The library never allocates or
+ * frees caller memory and keeps no per-call state; launches are
+ * asynchronous on `stream` and the caller synchronises.
+ *
+ * Conventions (identical to the reference):
+ *   HighwayHash key: 4 little-endian u64 lanes (S/highway.py:43-57).
+ *   SipHash key:     2 little-endian u64 words (S/sip.py:24-37).
+ *   Digests: u64 lanes, lane 0 first; width 64 -> 1 lane per message,
+ *   128 -> 2, 256 -> 4 (S/highway.py:223-234, 288-295).  Width 128 is not
+ *   defined by the reference (S/highway.py:228-229); here it is lanes 0-1 of
+ *   the 256-bit lane sum (derived, documented in DESIGN.md).
+ *   rounds: HighwayHash finalization rounds (reference default 4,
+ *   S/highway.py:223; tests use 1..3, T/test_backends.py:33-38).
+ *
+ * Return value: LH_OK (0) or a negative LH_E* code; lh_strerror() names it.
+ * The Python host maps LH_EINVAL/LH_EALIGN to ValueError (as the reference
+ * raises ValueError for bad widths/keys, S/highway.py:49-56, 228-229;
+ * S/sip.py:60-62) and the others to RuntimeError.
+ */
+#ifndef LANEHASH_B200_H
+#define LANEHASH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LH_OK 0
+#define LH_EINVAL (-1)   /* bad argument: width, rounds, c/d, NULL pointer */
+#define LH_EALIGN (-2)   /* misaligned output / offsets / lengths pointer */
+#define LH_ECUDA (-3)    /* CUDA runtime error (launch, attribute, ...) */
+#define LH_ENODEV (-4)   /* no usable sm_100 device */
+#define LH_ETOOBIG (-5)  /* size outside the supported range */
+
+/* Kernel selection for the *_kernel entry points (tests and bench force a
+ * path; the plain entry points choose automatically). */
+#define LH_KERNEL_AUTO 0
+#define LH_KERNEL_DIRECT 1 /* one thread per message, direct global loads */
+#define LH_KERNEL_TMA 2    /* TMA-staged shared-memory ring (fixed length) */
+
+/* Library / build identification. */
+const char* lh_version(void);
+const char* lh_strerror(int code);
+
+/* HighwayHash over n contiguous messages of `len` bytes each.
+ * Replaces: NumpyBackend.hash64_batch (S/backends.py:52-53 ->
+ * S/_highway_np.py:116-130), the numba batch _kernels.hash_batch(algo 0)
+ * (S/_kernels.py:268-274) and, at n = 1, backend.hash64/hash256
+ * (S/backends.py:28-33, 75-80).  d_out holds n * width/64 u64. */
+int lh_highway_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len,
+                     const uint64_t key[4], int width, int rounds,
+                     uint64_t* d_out, void* stream);
+int lh_highway_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
+                            const uint64_t key[4], int width, int rounds,
+                            uint64_t* d_out, void* stream, int kernel);
+
+/* HighwayHash over a packed ragged buffer: message i is
+ * d_buf[d_offsets[i] : d_offsets[i] + len_i], len_i = d_lengths[i] when
+ * d_lengths != NULL, else d_offsets[i+1] - d_offsets[i] (offsets has n+1
+ * entries).  Offsets are byte offsets with no alignment requirement.
+ * Replaces: per-message backend.hash64/hash256 (S/backends.py:22-80) over a
+ * batch of unequal lengths (the reference has no ragged API). */
+int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets,
+                      const uint32_t* d_lengths, uint64_t n,
+                      const uint64_t key[4], int width, int rounds,
+                      uint64_t* d_out, void* stream);
+
+/* SipHash-c-d (tree = 0) or SipTreeHash (tree = 1), n contiguous messages.
+ * Replaces: sip.siphash / sip.siptreehash (S/sip.py:89-128) and the numba
+ * _kernels.hash_batch algo 1 / 2 (S/_kernels.py:184-244, 268-274). */
+int lh_siphash_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len,
+                     const uint64_t key[2], int c, int d, int tree,
+                     uint64_t* d_out, void* stream);
+int lh_siphash_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
+                            const uint64_t key[2], int c, int d, int tree,
+                            uint64_t* d_out, void* stream, int kernel);
+int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets,
+                      const uint32_t* d_lengths, uint64_t n,
+                      const uint64_t key[2], int c, int d, int tree,
+                      uint64_t* d_out, void* stream);
+
+/* PRF mode: d_out[i] = HighwayHash-64(key, le64(start + i)), i < n.
+ * Composition of S/highway.py:247-249 over 8-byte counters (no input
+ * buffer). */
+int lh_highway_prf64(uint64_t start, uint64_t n, const uint64_t key[4],
+                     int rounds, uint64_t* d_out, void* stream);
+
+/* Seeded synthetic input generator (bench/test harness; not a reference
+ * interface).  Byte b of the stream is byte (b & 7) of
+ * word(seed, stream_id, word_offset + b / 8), see DESIGN.md §Synthetic
+ * inputs; fills nbytes bytes.  d_buf must be 8-byte aligned. */
+int lh_synth_fill(uint8_t* d_buf, uint64_t nbytes, uint64_t seed,
+                  uint64_t stream_id, uint64_t word_offset, void* stream);
+/* Lengths uniform in [lo, hi]: len[i] = lo + hi32(word(seed, 0, first+i)) *
+ * (hi - lo + 1) >> 32. */
+int lh_synth_lengths(uint32_t* d_len, uint64_t n, uint64_t seed,
+                     uint64_t first, uint32_t lo, uint32_t hi, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LANEHASH_B200_H */

@@ -1,0 +1,280 @@
+// lh_device.cuh — per-message hash state machines for the sm_100a engine.
+//
+// Everything here is integer work on registers: one message's whole state
+// lives in one thread.  The three "hashers" share one interface so the
+// message readers (TMA-staged shared memory, or direct global loads) can
+// feed any of them:
+//
+//   h.absorb32(p)            — one 32-byte block as 4 little-endian u64 words
+//   h.finish(t, r, len, out) — tail t (r = len % 32 bytes, zero beyond r)
+//
+// Semantics follow the reference package `lanehash` (S = pkg/src/lanehash):
+//   HighwayHash  S/highway.py:122-254   SipHash  S/sip.py:73-108
+//   SipTreeHash  S/sip.py:111-128
+#pragma once
+#include <stdint.h>
+
+namespace lh {
+
+typedef uint64_t u64;
+typedef uint32_t u32;
+
+__device__ __forceinline__ u32 lo32(u64 x) { return (u32)x; }
+__device__ __forceinline__ u32 hi32(u64 x) { return (u32)(x >> 32); }
+__device__ __forceinline__ u64 pack(u32 lo, u32 hi) {
+  return ((u64)hi << 32) | (u64)lo;
+}
+// Swapping the 32-bit halves is a register rename, not an instruction.
+__device__ __forceinline__ u64 rot32(u64 x) { return pack(hi32(x), lo32(x)); }
+
+// mul32 (S/highway.py:80-82): low32(a) * high32(b), full 64-bit product.
+// One IMAD.WIDE.U32.
+__device__ __forceinline__ u64 mul_lo_hi(u64 a, u64 b) {
+  return (u64)lo32(a) * (u64)hi32(b);
+}
+
+// Zipper merge of one lane pair (S/highway.py:35-38, 73-77).  Output byte i
+// of the 16-byte pair comes from input byte ZIP[i] = 3 C 2 5 E 1 F 0 B 4 A D
+// 9 6 8 7.  With input words W0..W3 (bytes 0-3, 4-7, 8-11, 12-15):
+//   R0 = [b3 b12 b2 b5]   R1 = [b14 b1 b15 b0]
+//   R2 = [b11 b4 b10 b13] R3 = [b9 b6 b8 b7]
+// which is 6 PRMT per pair.
+__device__ __forceinline__ void zipper(u64 lo, u64 hi, u64& zlo, u64& zhi) {
+  const u32 w0 = lo32(lo), w1 = hi32(lo), w2 = lo32(hi), w3 = hi32(hi);
+  const u32 r0 = __byte_perm(__byte_perm(w0, w3, 0x0243), w1, 0x5210);
+  const u32 r1 = __byte_perm(w3, w0, 0x4352);
+  const u32 r2 = __byte_perm(__byte_perm(w2, w1, 0x0243), w3, 0x5210);
+  const u32 r3 = __byte_perm(w2, w1, 0x7061);
+  zlo = pack(r0, r1);
+  zhi = pack(r2, r3);
+}
+
+// Key-only HighwayHash state (S/highway.py:122-127), expanded on the host and
+// passed by value as a kernel parameter (128 B).
+struct HHState {
+  u64 v0[4], v1[4], m0[4], m1[4];
+};
+
+struct Highway {
+  u64 v0[4], v1[4], m0[4], m1[4];
+  int rounds;
+  int width;  // 64, 128 or 256
+
+  __device__ __forceinline__ void init(const HHState& k, int rounds_, int width_) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v0[i] = k.v0[i];
+      v1[i] = k.v1[i];
+      m0[i] = k.m0[i];
+      m1[i] = k.m1[i];
+    }
+    rounds = rounds_;
+    width = width_;
+  }
+
+  // S/highway.py:130-150 — per-lane order of steps 1-5, then the two
+  // zipper-merge adds.
+  __device__ __forceinline__ void update(u64 p0, u64 p1, u64 p2, u64 p3) {
+    const u64 p[4] = {p0, p1, p2, p3};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v1[i] += p[i] + m0[i];
+      m0[i] ^= mul_lo_hi(v1[i], v0[i]);
+      v0[i] += m1[i];
+      m1[i] ^= mul_lo_hi(v0[i], v1[i]);
+    }
+    u64 z0, z1, z2, z3;
+    zipper(v1[0], v1[1], z0, z1);
+    zipper(v1[2], v1[3], z2, z3);
+    v0[0] += z0;
+    v0[1] += z1;
+    v0[2] += z2;
+    v0[3] += z3;
+    zipper(v0[0], v0[1], z0, z1);
+    zipper(v0[2], v0[3], z2, z3);
+    v1[0] += z0;
+    v1[1] += z1;
+    v1[2] += z2;
+    v1[3] += z3;
+  }
+
+  __device__ __forceinline__ void absorb32(const u64 (&p)[4]) {
+    update(p[0], p[1], p[2], p[3]);
+  }
+
+  // S/highway.py:182-220.  t holds the r tail bytes (zero beyond r).
+  __device__ __forceinline__ void remainder(const u64 (&t)[4], u32 r) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v0[i] = pack(lo32(v0[i]) + r, hi32(v0[i]) + r);
+      v1[i] = pack(__funnelshift_l(lo32(v1[i]), lo32(v1[i]), r),
+                   __funnelshift_l(hi32(v1[i]), hi32(v1[i]), r));
+    }
+    // Packet: tail[0 : 4*floor(r/4)], zeros, then the r%4 leftover bytes
+    // little-endian in packet bytes 28..31.
+    const u32 whole = r & ~3u;
+    u64 p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int keep = (int)whole - 8 * k;  // bytes of word k to keep
+      const u64 mask = keep >= 8 ? ~0ull : (keep <= 0 ? 0ull : ((1ull << (8 * keep)) - 1));
+      p[k] = t[k] & mask;
+    }
+    // whole is a multiple of 4: the leftover word starts on a 32-bit half.
+    // Select word whole/8 with two-level selects (keeps t in registers).
+    const u64 s01 = (whole & 8) ? t[1] : t[0];
+    const u64 s23 = (whole & 8) ? t[3] : t[2];
+    const u64 src = (whole & 16) ? s23 : s01;
+    u32 left = (whole & 4) ? hi32(src) : lo32(src);
+    const u32 nleft = r & 3u;
+    left &= nleft ? ((1u << (8 * nleft)) - 1u) : 0u;
+    p[3] |= (u64)left << 32;
+    update(p[0], p[1], p[2], p[3]);
+  }
+
+  // S/highway.py:176-179, 223-234.
+  __device__ __forceinline__ void finalize_rounds() {
+    for (int i = 0; i < rounds; ++i)
+      update(rot32(v0[2]), rot32(v0[3]), rot32(v0[0]), rot32(v0[1]));
+  }
+
+  // Writes width/64 lane sums; lane 0 is HighwayHash-64.
+  __device__ __forceinline__ void finish(const u64 (&t)[4], u32 r, u64 /*len*/,
+                                         u64* out) {
+    if (r) remainder(t, r);
+    finalize_rounds();
+    out[0] = v0[0] + v1[0] + m0[0] + m1[0];
+    if (width >= 128) out[1] = v0[1] + v1[1] + m0[1] + m1[1];
+    if (width == 256) {
+      out[2] = v0[2] + v1[2] + m0[2] + m1[2];
+      out[3] = v0[3] + v1[3] + m0[3] + m1[3];
+    }
+  }
+};
+
+// ---------------- SipHash-c-d (S/sip.py:73-108) ----------------
+
+__device__ __forceinline__ u64 rotl64(u64 x, int b) {
+  return (x << b) | (x >> (64 - b));
+}
+
+__device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3) {
+  v0 += v1;
+  v1 = rotl64(v1, 13) ^ v0;
+  v0 = rot32(v0);
+  v2 += v3;
+  v3 = rotl64(v3, 16) ^ v2;
+  v0 += v3;
+  v3 = rotl64(v3, 21) ^ v0;
+  v2 += v1;
+  v1 = rotl64(v1, 17) ^ v2;
+  v2 = rot32(v2);
+}
+
+struct SipKey {
+  u64 k0, k1;
+};
+
+// Round counts: compile-time when C,D > 0, else the runtime c,d fields.
+template <int C, int D>
+struct SipCore {
+  u64 v0, v1, v2, v3;
+  __device__ __forceinline__ void init(const SipKey& k) {
+    v0 = 0x736F6D6570736575ull ^ k.k0;
+    v1 = 0x646F72616E646F6Dull ^ k.k1;
+    v2 = 0x6C7967656E657261ull ^ k.k0;
+    v3 = 0x7465646279746573ull ^ k.k1;
+  }
+  __device__ __forceinline__ void compress(u64 m, int c) {
+    v3 ^= m;
+    if (C > 0) {
+#pragma unroll
+      for (int i = 0; i < C; ++i) sip_round(v0, v1, v2, v3);
+    } else {
+      for (int i = 0; i < c; ++i) sip_round(v0, v1, v2, v3);
+    }
+    v0 ^= m;
+  }
+  __device__ __forceinline__ u64 final(u64 m_last, int c, int d) {
+    compress(m_last, c);
+    v2 ^= 0xFF;
+    if (D > 0) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) sip_round(v0, v1, v2, v3);
+    } else {
+      for (int i = 0; i < d; ++i) sip_round(v0, v1, v2, v3);
+    }
+    return v0 ^ v1 ^ v2 ^ v3;
+  }
+};
+
+template <int C, int D>
+struct Sip {
+  SipCore<C, D> s;
+  int c, d;
+  __device__ __forceinline__ void init(const SipKey& k, int c_, int d_) {
+    s.init(k);
+    c = c_;
+    d = d_;
+  }
+  __device__ __forceinline__ void absorb32(const u64 (&p)[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s.compress(p[k], c);
+  }
+  // Tail: r = len % 32 bytes in t (zero beyond r).  Whole words first, then
+  // the final word = leftover bytes | (len & 0xFF) << 56 (S/sip.py:100-101).
+  __device__ __forceinline__ void finish(const u64 (&t)[4], u32 r, u64 len, u64* out) {
+    const u32 nw = r >> 3;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if ((u32)k < nw) s.compress(t[k], c);
+    const u64 s01 = (nw & 1) ? t[1] : t[0];
+    const u64 s23 = (nw & 1) ? t[3] : t[2];
+    const u64 last = (nw & 2) ? s23 : s01;
+    out[0] = s.final(last | ((len & 0xFF) << 56), c, d);
+  }
+};
+
+// SipTreeHash (S/sip.py:111-128): the zero-padded message's 64-bit words are
+// dealt round-robin to 4 independent SipHash chains (ILP 4 in one thread);
+// each chain's own length is padded_len/4; the 4 digests are folded with one
+// more SipHash over their 32-byte little-endian concatenation.
+template <int C, int D>
+struct SipTree {
+  SipCore<C, D> l0, l1, l2, l3;
+  SipKey key;
+  int c, d;
+  __device__ __forceinline__ void init(const SipKey& k, int c_, int d_) {
+    key = k;
+    l0.init(k);
+    l1.init(k);
+    l2.init(k);
+    l3.init(k);
+    c = c_;
+    d = d_;
+  }
+  __device__ __forceinline__ void absorb32(const u64 (&p)[4]) {
+    l0.compress(p[0], c);
+    l1.compress(p[1], c);
+    l2.compress(p[2], c);
+    l3.compress(p[3], c);
+  }
+  __device__ __forceinline__ void finish(const u64 (&t)[4], u32 r, u64 len, u64* out) {
+    if (r) absorb32(t);  // zero-padded final block
+    const u64 lane_len = ((len + 31) & ~31ull) >> 2;
+    const u64 m = (lane_len & 0xFF) << 56;
+    const u64 h0 = l0.final(m, c, d);
+    const u64 h1 = l1.final(m, c, d);
+    const u64 h2 = l2.final(m, c, d);
+    const u64 h3 = l3.final(m, c, d);
+    SipCore<C, D> f;
+    f.init(key);
+    f.compress(h0, c);
+    f.compress(h1, c);
+    f.compress(h2, c);
+    f.compress(h3, c);
+    out[0] = f.final(32ull << 56, c, d);
+  }
+};
+
+}  // namespace lh

@@ -1,0 +1,578 @@
+// lh_engine.cu — sm_100a kernels and the extern "C" boundary
+// (include/lanehash_b200.h).
+//
+// Kernels:
+//   k_tma_fixed<H,ROWS,STAGES>  fixed-length batch; one thread per message;
+//       a producer warp streams ROWS x 128-byte boxes of the (n, len) byte
+//       matrix into a STAGES-deep shared-memory ring with 2-D TMA
+//       (SWIZZLE_128B, so each thread's 16-byte reads of its own row are
+//       bank-conflict free); consumer threads run the hash on registers.
+//   k_direct<H>  any layout (fixed or ragged, any alignment/length); one
+//       thread per message reading its bytes with 8-byte-aligned loads and
+//       funnel shifts.
+//   k_prf        HighwayHash-64 of 8-byte LE counters (no input bytes).
+// H is one of lh::Highway, lh::Sip<C,D>, lh::SipTree<C,D> (lh_device.cuh).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/lanehash_b200.h"
+#include "lh_device.cuh"
+#include "lh_tma.cuh"
+
+using namespace lh;
+
+#define LH_VERSION_STR "paper_1612_06257_b200 0.1.0 (sm_100a)"
+
+namespace {
+
+// --------------------------------------------------------------------------
+// Host-side hasher prototypes (the kernels copy them by value).
+// --------------------------------------------------------------------------
+
+// S/highway.py:20-31
+const u64 kInit0[4] = {0xDBE6D5D5FE4CCE2FULL, 0xA4093822299F31D0ULL, 0x13198A2E03707344ULL,
+                       0x243F6A8885A308D3ULL};
+const u64 kInit1[4] = {0x3BD39E10CB0EF593ULL, 0xC0ACF169B5F18A8CULL, 0xBE5466CF34E90C6CULL,
+                       0x452821E638D01377ULL};
+
+inline u64 h_rot32(u64 x) { return (x >> 32) | (x << 32); }
+
+// Key expansion, S/highway.py:122-127 (one key per batch: done once here).
+Highway make_highway(const u64 key[4], int width, int rounds) {
+  Highway h;
+  memset(&h, 0, sizeof h);
+  for (int i = 0; i < 4; ++i) {
+    h.v0[i] = key[i] ^ kInit0[i];
+    h.v1[i] = h_rot32(key[i]) ^ kInit1[i];
+    h.m0[i] = kInit0[i];
+    h.m1[i] = kInit1[i];
+  }
+  h.rounds = rounds;
+  h.width = width;
+  return h;
+}
+
+template <int C, int D>
+void h_sip_init(SipCore<C, D>& s, const SipKey& k) {
+  s.v0 = 0x736F6D6570736575ull ^ k.k0;
+  s.v1 = 0x646F72616E646F6Dull ^ k.k1;
+  s.v2 = 0x6C7967656E657261ull ^ k.k0;
+  s.v3 = 0x7465646279746573ull ^ k.k1;
+}
+
+template <int C, int D>
+Sip<C, D> make_sip(const u64 key[2], int c, int d) {
+  Sip<C, D> h;
+  memset(&h, 0, sizeof h);
+  h_sip_init(h.s, SipKey{key[0], key[1]});
+  h.c = c;
+  h.d = d;
+  return h;
+}
+
+template <int C, int D>
+SipTree<C, D> make_siptree(const u64 key[2], int c, int d) {
+  SipTree<C, D> h;
+  memset(&h, 0, sizeof h);
+  const SipKey k{key[0], key[1]};
+  h.key = k;
+  h_sip_init(h.l0, k);
+  h_sip_init(h.l1, k);
+  h_sip_init(h.l2, k);
+  h_sip_init(h.l3, k);
+  h.c = c;
+  h.d = d;
+  return h;
+}
+
+template <class H>
+__host__ __device__ inline int nout(const H&) {
+  return 1;
+}
+template <>
+__host__ __device__ inline int nout<Highway>(const Highway& h) {
+  return h.width / 64;
+}
+
+// --------------------------------------------------------------------------
+// Direct (global-load) reader: any alignment, any length, fixed or ragged.
+// Only 8-byte-aligned words that contain at least one message byte are
+// read, so no access leaves the message's own aligned words.
+// --------------------------------------------------------------------------
+
+__device__ __forceinline__ u64 ldg64(const u64* p) { return __ldg((const unsigned long long*)p); }
+
+__device__ __forceinline__ u64 funnel(u64 a, u64 b, u32 sh) {
+  // bytes of the 16-byte window a|b starting at byte sh/8 (sh in 8..56)
+  return (a >> sh) | (b << (64 - sh));
+}
+
+__device__ __forceinline__ void mask_tail(u64 (&t)[4], u32 r) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int keep = (int)r - 8 * k;
+    const u64 m = keep >= 8 ? ~0ull : (keep <= 0 ? 0ull : ((1ull << (8 * keep)) - 1));
+    t[k] &= m;
+  }
+}
+
+template <class H>
+__device__ __forceinline__ void hash_direct(H& h, const uint8_t* msg, u64 len, u64* out) {
+  const u64 full = len & ~31ull;
+  const u32 r = (u32)(len & 31);
+  const uintptr_t a = (uintptr_t)msg;
+  const u32 sh = (u32)(a & 7) * 8;
+  const u64* w = (const u64*)(a & ~(uintptr_t)7);
+  u64 t[4] = {0, 0, 0, 0};
+  if (sh == 0) {
+    if ((a & 15) == 0) {
+      const ulonglong2* w2 = (const ulonglong2*)w;
+      for (u64 b = 0; b < (full >> 5); ++b) {
+        const ulonglong2 x = __ldg(w2 + 2 * b);
+        const ulonglong2 y = __ldg(w2 + 2 * b + 1);
+        const u64 p[4] = {x.x, x.y, y.x, y.y};
+        h.absorb32(p);
+      }
+    } else {
+      for (u64 b = 0; b < (full >> 5); ++b) {
+        const u64 p[4] = {ldg64(w + 4 * b), ldg64(w + 4 * b + 1), ldg64(w + 4 * b + 2),
+                          ldg64(w + 4 * b + 3)};
+        h.absorb32(p);
+      }
+    }
+    if (r) {
+      const u64* tw = w + (full >> 3);
+      const u32 nw = (r + 7) >> 3;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((u32)k < nw) t[k] = ldg64(tw + k);
+      mask_tail(t, r);
+    }
+  } else {
+    u64 cur = len ? ldg64(w) : 0;
+    for (u64 b = 0; b < (full >> 5); ++b) {
+      const u64* q = w + 4 * b;
+      const u64 n0 = ldg64(q + 1), n1 = ldg64(q + 2), n2 = ldg64(q + 3), n3 = ldg64(q + 4);
+      const u64 p[4] = {funnel(cur, n0, sh), funnel(n0, n1, sh), funnel(n1, n2, sh),
+                        funnel(n2, n3, sh)};
+      cur = n3;
+      h.absorb32(p);
+    }
+    if (r) {
+      // words covering [a+full, a+full+r): cur plus `extra` more.
+      const u64 first = (a + full) >> 3;
+      const u32 extra = (u32)(((a + full + r - 1) >> 3) - first);
+      const u64* q = w + (full >> 3);
+      u64 W[5];
+      W[0] = cur;
+#pragma unroll
+      for (int k = 1; k < 5; ++k) W[k] = ((u32)k <= extra) ? ldg64(q + k) : 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) t[k] = funnel(W[k], W[k + 1], sh);
+      mask_tail(t, r);
+    }
+  }
+  h.finish(t, r, len, out);
+}
+
+template <class H>
+__global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __restrict__ buf,
+                                                const u64* __restrict__ offsets,
+                                                const u32* __restrict__ lengths, u64 fixed_len,
+                                                u64 n, u64* __restrict__ out) {
+  const int W = nout(proto);
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    const uint8_t* msg;
+    u64 len;
+    if (offsets) {
+      const u64 off = offsets[i];
+      len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
+      msg = buf + off;
+    } else {
+      msg = buf + i * fixed_len;
+      len = fixed_len;
+    }
+    H h = proto;
+    hash_direct(h, msg, len, out + i * W);
+  }
+}
+
+// --------------------------------------------------------------------------
+// TMA-staged fixed-length kernel.
+// Requirements (checked on the host): len % 16 == 0, d_msgs 16-B aligned.
+// Shared ring: STAGES x [ROWS rows x 128 B] with the 128-byte swizzle:
+// 16-byte unit u of row t lives at t*128 + ((u ^ (t & 7)) << 4).
+// --------------------------------------------------------------------------
+
+constexpr int kBoxBytes = 128;
+
+template <int ROWS, int STAGES>
+constexpr size_t tma_smem_bytes() {
+  return 1024 /*alignment slack*/ + (size_t)STAGES * ROWS * kBoxBytes + 2 * STAGES * 8;
+}
+
+template <class H, int ROWS, int STAGES, int MINB>
+__global__ void __launch_bounds__(ROWS + 32, MINB)
+    k_tma_fixed(const __grid_constant__ CUtensorMap tmap, const H proto, u64 n, u64 len,
+                u64* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr u32 kStageBytes = ROWS * kBoxBytes;
+  constexpr int kConsumerWarps = ROWS / 32;
+  uint64_t* full_bar = (uint64_t*)(smem + STAGES * kStageBytes);
+  uint64_t* empty_bar = full_bar + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const u64 ntiles = (n + ROWS - 1) / ROWS;
+  const u32 nchunks = (u32)((len + kBoxBytes - 1) / kBoxBytes);
+
+  if (warp == kConsumerWarps) {
+    // ---- producer: one elected lane streams boxes into the ring ----
+    if (lane == 0) {
+      tma_prefetch_desc(&tmap);
+      u32 it = 0;
+      for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (u32 c = 0; c < nchunks; ++c, ++it) {
+          const u32 s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
+          tma_load_2d(smem + s * kStageBytes, &tmap, (int32_t)(c * kBoxBytes),
+                      (int32_t)(tile * ROWS), &full_bar[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: thread t owns message row tile*ROWS + t ----
+  const u32 t = threadIdx.x;
+  const u32 sw = t & 7;
+  const int W = nout(proto);
+  const u64 nfull = len >> 5;
+  const u32 r = (u32)(len & 31);  // 0 or 16
+  u32 it = 0;
+  for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    H h = proto;
+    u64 tl[4] = {0, 0, 0, 0};
+    for (u32 c = 0; c < nchunks; ++c, ++it) {
+      const u32 s = it % STAGES, ph = (it / STAGES) & 1;
+      mbar_wait(&full_bar[s], ph);
+      const uint8_t* row = smem + s * kStageBytes + t * kBoxBytes;
+      const u64 left = nfull - (u64)c * 4;
+      const u32 kvalid = left >= 4 ? 4u : (u32)left;
+      if (kvalid == 4) {
+#pragma unroll
+        for (u32 k = 0; k < 4; ++k) {
+          const uint4 a = lds128(row + (((2 * k) ^ sw) << 4));
+          const uint4 b = lds128(row + (((2 * k + 1) ^ sw) << 4));
+          const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
+          h.absorb32(p);
+        }
+      } else {
+        for (u32 k = 0; k < kvalid; ++k) {
+          const uint4 a = lds128(row + (((2 * k) ^ sw) << 4));
+          const uint4 b = lds128(row + (((2 * k + 1) ^ sw) << 4));
+          const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
+          h.absorb32(p);
+        }
+        if (r) {
+          const uint4 a = lds128(row + (((2 * kvalid) ^ sw) << 4));
+          tl[0] = pack(a.x, a.y);
+          tl[1] = pack(a.z, a.w);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+    const u64 row_idx = tile * ROWS + t;
+    if (row_idx < n) h.finish(tl, r, len, out + row_idx * W);
+  }
+}
+
+// --------------------------------------------------------------------------
+// PRF: hash64(key, le64(ctr)).  With r = 8 the remainder packet is
+// (ctr, 0, 0, 0) (S/highway.py:206-220) and the length injection is
+// key-only, so `proto` arrives already tweaked; per counter: 1 + rounds
+// updates.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_prf(const Highway proto, u64 start, u64 n,
+                                             u64* __restrict__ out) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    Highway h = proto;
+    h.update(start + i, 0, 0, 0);
+    h.finalize_rounds();
+    out[i] = h.v0[0] + h.v1[0] + h.m0[0] + h.m1[0];
+  }
+}
+
+// --------------------------------------------------------------------------
+// Host helpers
+// --------------------------------------------------------------------------
+
+int cuda_err(cudaError_t e) { return e == cudaSuccess ? LH_OK : LH_ECUDA; }
+
+int check_device(int* sms) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return LH_ENODEV;
+  int major = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+    return LH_ENODEV;
+  if (major < 10) return LH_ENODEV;
+  if (sms && cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return LH_ENODEV;
+  return LH_OK;
+}
+
+unsigned grid_for(u64 n, int threads, int sms) {
+  const u64 blocks = (n + threads - 1) / threads;
+  const u64 cap = (u64)sms * 64;  // grid-stride beyond 64 waves' worth
+  return (unsigned)(blocks < cap ? (blocks ? blocks : 1) : cap);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+template <class H>
+int launch_direct(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths,
+                  u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  k_direct<H><<<grid_for(n, 256, sms), 256, 0, st>>>(proto, buf, offsets, lengths, fixed_len,
+                                                     n, out);
+  return cuda_err(cudaGetLastError());
+}
+
+template <class H, int ROWS, int STAGES, int MINB>
+int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
+                   cudaStream_t st, int sms) {
+  auto enc = get_encode();
+  if (!enc) return LH_ECUDA;
+  constexpr size_t smem = tma_smem_bytes<ROWS, STAGES>();
+  auto kern = k_tma_fixed<H, ROWS, STAGES, MINB>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return LH_ECUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ROWS + 32, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return LH_ECUDA;
+  // Rows are split into segments of < 2^31 (TMA coordinates are int32).
+  const u64 kSeg = 1ull << 30;
+  const int W = nout(proto);
+  for (u64 base = 0; base < n; base += kSeg) {
+    const u64 nn = n - base < kSeg ? n - base : kSeg;
+    CUtensorMap map;
+    cuuint64_t dims[2] = {(cuuint64_t)len, (cuuint64_t)nn};
+    cuuint64_t strides[1] = {(cuuint64_t)len};
+    cuuint32_t box[2] = {(cuuint32_t)kBoxBytes, (cuuint32_t)ROWS};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)(msgs + base * len), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return LH_ECUDA;
+    const u64 tiles = (nn + ROWS - 1) / ROWS;
+    const u64 cap = (u64)sms * per_sm;
+    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+    kern<<<grid, ROWS + 32, smem, st>>>(map, proto, nn, len, out + base * W);
+    int rc = cuda_err(cudaGetLastError());
+    if (rc) return rc;
+  }
+  return LH_OK;
+}
+
+template <class H>
+int launch_tma(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out, cudaStream_t st) {
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  // Long messages with few rows: 32-row tiles keep more SMs busy.
+  if (n < (u64)sms * 3 * 128) return launch_tma_cfg<H, 32, 8, 4>(proto, msgs, n, len, out, st, sms);
+  return launch_tma_cfg<H, 128, 4, 3>(proto, msgs, n, len, out, st, sms);
+}
+
+bool tma_ok(const uint8_t* msgs, u64 n, u64 len) {
+  return len >= 32 && (len % 16) == 0 && ((uintptr_t)msgs % 16) == 0 && len < (1ull << 31) &&
+         n > 0;
+}
+
+template <class H>
+int dispatch_fixed(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
+                   cudaStream_t st, int kernel) {
+  if (kernel == LH_KERNEL_TMA) {
+    if (n && !tma_ok(msgs, n, len)) return LH_EINVAL;
+    return launch_tma(proto, msgs, n, len, out, st);
+  }
+  if (kernel == LH_KERNEL_AUTO && tma_ok(msgs, n, len) && n >= 1024)
+    return launch_tma(proto, msgs, n, len, out, st);
+  return launch_direct(proto, msgs, nullptr, nullptr, len, n, out, st);
+}
+
+bool valid_width(int w) { return w == 64 || w == 128 || w == 256; }
+
+template <class H>
+int sip_dispatch_ragged(const H& h, const uint8_t* buf, const u64* off, const u32* lens, u64 n,
+                        u64* out, cudaStream_t st) {
+  return launch_direct(h, buf, off, lens, 0, n, out, st);
+}
+
+}  // namespace
+
+// ==========================================================================
+// extern "C" boundary
+// ==========================================================================
+extern "C" {
+
+const char* lh_version(void) { return LH_VERSION_STR; }
+
+const char* lh_strerror(int code) {
+  switch (code) {
+    case LH_OK: return "ok";
+    case LH_EINVAL: return "invalid argument";
+    case LH_EALIGN: return "misaligned pointer";
+    case LH_ECUDA: return "CUDA runtime error";
+    case LH_ENODEV: return "no sm_100 CUDA device";
+    case LH_ETOOBIG: return "size out of supported range";
+    default: return "unknown error";
+  }
+}
+
+int lh_highway_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
+                            const uint64_t key[4], int width, int rounds, uint64_t* d_out,
+                            void* stream, int kernel) {
+  if (!key || !valid_width(width) || rounds < 0 || (n && !d_out) || (n && len && !d_msgs))
+    return LH_EINVAL;
+  if ((uintptr_t)d_out % 8) return LH_EALIGN;
+  if (kernel < 0 || kernel > LH_KERNEL_TMA) return LH_EINVAL;
+  if (len && n > UINT64_MAX / len) return LH_ETOOBIG;
+  const Highway h = make_highway(key, width, rounds);
+  return dispatch_fixed(h, d_msgs, n, len, d_out, (cudaStream_t)stream, kernel);
+}
+
+int lh_highway_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len, const uint64_t key[4],
+                     int width, int rounds, uint64_t* d_out, void* stream) {
+  return lh_highway_fixed_kernel(d_msgs, n, len, key, width, rounds, d_out, stream,
+                                 LH_KERNEL_AUTO);
+}
+
+int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,
+                      uint64_t n, const uint64_t key[4], int width, int rounds, uint64_t* d_out,
+                      void* stream) {
+  if (!key || !valid_width(width) || rounds < 0 || (n && (!d_out || !d_offsets || !d_buf)))
+    return LH_EINVAL;
+  if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
+    return LH_EALIGN;
+  const Highway h = make_highway(key, width, rounds);
+  return launch_direct(h, d_buf, d_offsets, d_lengths, 0, n, d_out, (cudaStream_t)stream);
+}
+
+static int sip_fixed_impl(const uint8_t* d_msgs, u64 n, u64 len, const u64 key[2], int c, int d,
+                          int tree, u64* d_out, cudaStream_t st, int kernel) {
+  if (tree) {
+    if (c == 2 && d == 4)
+      return dispatch_fixed(make_siptree<2, 4>(key, c, d), d_msgs, n, len, d_out, st, kernel);
+    if (c == 1 && d == 3)
+      return dispatch_fixed(make_siptree<1, 3>(key, c, d), d_msgs, n, len, d_out, st, kernel);
+    return dispatch_fixed(make_siptree<0, 0>(key, c, d), d_msgs, n, len, d_out, st, kernel);
+  }
+  if (c == 2 && d == 4)
+    return dispatch_fixed(make_sip<2, 4>(key, c, d), d_msgs, n, len, d_out, st, kernel);
+  if (c == 1 && d == 3)
+    return dispatch_fixed(make_sip<1, 3>(key, c, d), d_msgs, n, len, d_out, st, kernel);
+  return dispatch_fixed(make_sip<0, 0>(key, c, d), d_msgs, n, len, d_out, st, kernel);
+}
+
+int lh_siphash_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
+                            const uint64_t key[2], int c, int d, int tree, uint64_t* d_out,
+                            void* stream, int kernel) {
+  if (!key || c < 1 || d < 1 || (n && !d_out) || (n && len && !d_msgs)) return LH_EINVAL;
+  if ((uintptr_t)d_out % 8) return LH_EALIGN;
+  if (kernel < 0 || kernel > LH_KERNEL_TMA) return LH_EINVAL;
+  if (len && n > UINT64_MAX / len) return LH_ETOOBIG;
+  return sip_fixed_impl(d_msgs, n, len, key, c, d, tree, d_out, (cudaStream_t)stream, kernel);
+}
+
+int lh_siphash_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len, const uint64_t key[2],
+                     int c, int d, int tree, uint64_t* d_out, void* stream) {
+  return lh_siphash_fixed_kernel(d_msgs, n, len, key, c, d, tree, d_out, stream,
+                                 LH_KERNEL_AUTO);
+}
+
+int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,
+                      uint64_t n, const uint64_t key[2], int c, int d, int tree, uint64_t* d_out,
+                      void* stream) {
+  if (!key || c < 1 || d < 1 || (n && (!d_out || !d_offsets || !d_buf))) return LH_EINVAL;
+  if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
+    return LH_EALIGN;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tree) {
+    if (c == 2 && d == 4)
+      return sip_dispatch_ragged(make_siptree<2, 4>(key, c, d), d_buf, d_offsets, d_lengths, n,
+                                 d_out, st);
+    if (c == 1 && d == 3)
+      return sip_dispatch_ragged(make_siptree<1, 3>(key, c, d), d_buf, d_offsets, d_lengths, n,
+                                 d_out, st);
+    return sip_dispatch_ragged(make_siptree<0, 0>(key, c, d), d_buf, d_offsets, d_lengths, n,
+                               d_out, st);
+  }
+  if (c == 2 && d == 4)
+    return sip_dispatch_ragged(make_sip<2, 4>(key, c, d), d_buf, d_offsets, d_lengths, n, d_out,
+                               st);
+  if (c == 1 && d == 3)
+    return sip_dispatch_ragged(make_sip<1, 3>(key, c, d), d_buf, d_offsets, d_lengths, n, d_out,
+                               st);
+  return sip_dispatch_ragged(make_sip<0, 0>(key, c, d), d_buf, d_offsets, d_lengths, n, d_out,
+                             st);
+}
+
+int lh_highway_prf64(uint64_t start, uint64_t n, const uint64_t key[4], int rounds,
+                     uint64_t* d_out, void* stream) {
+  if (!key || rounds < 0 || (n && !d_out)) return LH_EINVAL;
+  if ((uintptr_t)d_out % 8) return LH_EALIGN;
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  Highway h = make_highway(key, 64, rounds);
+  // Length injection for r = 8 (S/highway.py:188-197), key-only.
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t lo = (uint32_t)h.v0[i] + 8u, hi = (uint32_t)(h.v0[i] >> 32) + 8u;
+    h.v0[i] = ((u64)hi << 32) | lo;
+    const uint32_t l1 = (uint32_t)h.v1[i], h1 = (uint32_t)(h.v1[i] >> 32);
+    const uint32_t rl = (l1 << 8) | (l1 >> 24), rh = (h1 << 8) | (h1 >> 24);
+    h.v1[i] = ((u64)rh << 32) | rl;
+  }
+  k_prf<<<grid_for(n, 256, sms), 256, 0, (cudaStream_t)stream>>>(h, start, n, d_out);
+  return cuda_err(cudaGetLastError());
+}
+
+}  // extern "C"

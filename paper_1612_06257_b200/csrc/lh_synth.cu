@@ -1,0 +1,92 @@
+// lh_synth.cu — seeded counter-based synthetic input generator (harness).
+//
+// word(seed, stream, w) = mix64(k + (w + 1) * G), k = mix64(seed * G + stream + 1),
+// G = 0x9E3779B97F4A7C15, mix64 = the SplitMix64 finalizer.  Byte b of a
+// generated buffer is byte (b & 7) (little-endian) of word(b >> 3).  The
+// numpy twin is paper_1612_06257_b200/synth.py; tests cross-check them.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lanehash_b200.h"
+
+namespace {
+
+constexpr uint64_t kG = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_fill(uint64_t* __restrict__ dst, uint64_t nwords, uint64_t key,
+                       uint64_t word_offset) {
+  // 2 words per thread-iteration with 16-byte stores where possible.
+  const uint64_t npairs = nwords / 2;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t w = word_offset + 2 * i;
+    ulonglong2 v;
+    v.x = mix64(key + (w + 1) * kG);
+    v.y = mix64(key + (w + 2) * kG);
+    if (((uintptr_t)dst & 15) == 0) {
+      reinterpret_cast<ulonglong2*>(dst)[i] = v;
+    } else {
+      dst[2 * i] = v.x;
+      dst[2 * i + 1] = v.y;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (nwords & 1)) {
+    const uint64_t w = word_offset + nwords - 1;
+    dst[nwords - 1] = mix64(key + (w + 1) * kG);
+  }
+}
+
+__global__ void k_tail(uint8_t* dst, uint64_t nbytes, uint64_t key, uint64_t word_offset) {
+  const uint64_t wi = nbytes >> 3;
+  const uint64_t v = mix64(key + (word_offset + wi + 1) * kG);
+  for (uint64_t b = wi * 8; b < nbytes; ++b) dst[b] = (uint8_t)(v >> (8 * (b & 7)));
+}
+
+__global__ void k_lengths(uint32_t* __restrict__ out, uint64_t n, uint64_t key, uint64_t first,
+                          uint32_t lo, uint32_t span) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = mix64(key + (first + i + 1) * kG);
+    out[i] = lo + (uint32_t)(((v >> 32) * (uint64_t)span) >> 32);
+  }
+}
+
+unsigned grid(uint64_t items) {
+  const uint64_t b = (items + 255) / 256;
+  return (unsigned)(b == 0 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
+
+}  // namespace
+
+extern "C" {
+
+int lh_synth_fill(uint8_t* d_buf, uint64_t nbytes, uint64_t seed, uint64_t stream_id,
+                  uint64_t word_offset, void* stream) {
+  if (nbytes && !d_buf) return LH_EINVAL;
+  if ((uintptr_t)d_buf % 8) return LH_EALIGN;
+  if (!nbytes) return LH_OK;
+  const uint64_t key = mix64(seed * kG + stream_id + 1);
+  const uint64_t nwords = nbytes >> 3;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nwords) k_fill<<<grid(nwords / 2 + 1), 256, 0, st>>>((uint64_t*)d_buf, nwords, key, word_offset);
+  if (nbytes & 7) k_tail<<<1, 1, 0, st>>>(d_buf, nbytes, key, word_offset);
+  return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
+}
+
+int lh_synth_lengths(uint32_t* d_len, uint64_t n, uint64_t seed, uint64_t first, uint32_t lo,
+                     uint32_t hi, void* stream) {
+  if ((n && !d_len) || hi < lo) return LH_EINVAL;
+  if ((uintptr_t)d_len % 4) return LH_EALIGN;
+  if (!n) return LH_OK;
+  const uint64_t key = mix64(seed * kG + 0 + 1);
+  k_lengths<<<grid(n), 256, 0, (cudaStream_t)stream>>>(d_len, n, key, first, lo, hi - lo + 1);
+  return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,275 @@
+"""Batch API of the B200 engine (the hot path behind the reference interface).
+
+All functions take either CUDA tensors (zero-copy: the call is a single
+asynchronous kernel launch on the current stream; results stay in HBM) or
+host arrays (numpy / CPU torch tensors; the call streams the batch through
+the GPU in chunks — H2D, kernel and D2H overlapped on two CUDA streams —
+and returns host numpy ``uint64`` digests).
+
+Digests are 64-bit words stored in ``torch.int64`` tensors on the device
+(bit-identical to uint64; ``to_u64`` converts to numpy ``uint64``).  Layout:
+width 64 -> shape (n,), 128 -> (n, 2), 256 -> (n, 4), lane 0 first.
+
+Reference correspondence (S = /root/reference/pkg/src/lanehash):
+  highway_batch  <- NumpyBackend.hash64_batch (S/backends.py:52-53,
+                    S/_highway_np.py:116-130), _kernels.hash_batch algo 0
+                    (S/_kernels.py:268-274), widths 64/128/256
+  highway_ragged <- per-message hash64/hash256 over unequal lengths
+  sip_batch      <- _kernels.hash_batch algo 1/2 (S/_kernels.py:237-244),
+                    sip.siphash / sip.siptreehash (S/sip.py:89-128)
+  prf64          <- hash64(key, le64(ctr)) (S/highway.py:247-249)
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .highway import Key256, _check_width, as_key256
+from .sip import Key128, as_key128
+
+KERNEL_AUTO = _lib.KERNEL_AUTO
+KERNEL_DIRECT = _lib.KERNEL_DIRECT
+KERNEL_TMA = _lib.KERNEL_TMA
+
+#: Host-path chunk size (bytes of message payload per H2D copy).
+HOST_CHUNK_BYTES = 128 << 20
+
+
+def _require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.EngineError("no CUDA device: the B200 engine has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _key4(key: Key256):
+    return (ctypes.c_uint64 * 4)(*key.lanes)
+
+
+def _key2(key: Key128):
+    return (ctypes.c_uint64 * 2)(key.k0, key.k1)
+
+
+def to_u64(t) -> np.ndarray:
+    """Digest tensor/array -> numpy uint64 (bit-preserving)."""
+    if isinstance(t, torch.Tensor):
+        t = t.detach().cpu().numpy()
+    return np.asarray(t).view(np.uint64)
+
+
+def _as_u8_2d(msgs):
+    if isinstance(msgs, torch.Tensor):
+        if msgs.dtype != torch.uint8 or msgs.dim() != 2:
+            raise ValueError("messages must be a 2-D uint8 tensor (n, length)")
+        return msgs
+    a = np.asarray(msgs)
+    if a.dtype != np.uint8 or a.ndim != 2:
+        raise ValueError("messages must be a 2-D uint8 array (n, length)")
+    return torch.from_numpy(np.ascontiguousarray(a))
+
+
+def _out_shape(n: int, lanes: int):
+    return (n,) if lanes == 1 else (n, lanes)
+
+
+# ---------------------------------------------------------------------------
+# Fixed-length batches
+# ---------------------------------------------------------------------------
+
+def _launch_fixed(kind, key, d_msgs: torch.Tensor, n: int, L: int, p1: int, p2: int,
+                  tree: int, d_out: torch.Tensor, kernel: int, device) -> None:
+    st = _stream_ptr(device)
+    ptr = d_msgs.data_ptr() if d_msgs.numel() else 0
+    if kind == "hh":
+        rc = _lib.lib().lh_highway_fixed_kernel(ptr, n, L, _key4(key), p1, p2,
+                                                d_out.data_ptr(), st, kernel)
+        _lib.check(rc, "lh_highway_fixed")
+    else:
+        rc = _lib.lib().lh_siphash_fixed_kernel(ptr, n, L, _key2(key), p1, p2, tree,
+                                                d_out.data_ptr(), st, kernel)
+        _lib.check(rc, "lh_siphash_fixed")
+
+
+def _fixed(kind, key, msgs, p1, p2, tree, lanes, kernel, out=None):
+    device = _require_cuda()
+    m = _as_u8_2d(msgs)
+    n, L = m.shape
+    if m.is_cuda:
+        m = m.contiguous()
+        if out is None:
+            out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=m.device)
+        if n:
+            with torch.cuda.device(m.device):
+                _launch_fixed(kind, key, m, n, L, p1, p2, tree, out, kernel, m.device)
+        return out
+    return _fixed_host(kind, key, m.contiguous(), p1, p2, tree, lanes, kernel, device)
+
+
+def _fixed_host(kind, key, m: torch.Tensor, p1, p2, tree, lanes, kernel, device):
+    """Stream a host (n, L) batch through the GPU: per chunk, H2D -> kernel ->
+    D2H on alternating streams so copies overlap the other chunk's kernel."""
+    n, L = m.shape
+    out_host = torch.empty(_out_shape(n, lanes), dtype=torch.int64,
+                           pin_memory=torch.cuda.is_available())
+    if n == 0:
+        return to_u64(out_host)
+    rows = n if L == 0 else max(1, min(n, HOST_CHUNK_BYTES // L))
+    if rows < n and rows >= 128:
+        rows -= rows % 128
+    streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
+    cur = torch.cuda.current_stream(device)
+    nbuf = 2 if rows < n else 1
+    dbuf = [torch.empty((rows, L), dtype=torch.uint8, device=device) for _ in range(nbuf)]
+    dout = [torch.empty(_out_shape(rows, lanes), dtype=torch.int64, device=device)
+            for _ in range(nbuf)]
+    for s in streams:
+        s.wait_stream(cur)
+    for k, r0 in enumerate(range(0, n, rows)):
+        r1 = min(n, r0 + rows)
+        s = streams[k % 2]
+        b = k % nbuf
+        with torch.cuda.stream(s):
+            db = dbuf[b][: r1 - r0]
+            db.copy_(m[r0:r1], non_blocking=True)
+            do = dout[b][: r1 - r0]
+            _launch_fixed(kind, key, db, r1 - r0, L, p1, p2, tree, do, kernel, device)
+            out_host[r0:r1].copy_(do, non_blocking=True)
+    for s in streams:
+        s.synchronize()
+    return to_u64(out_host)
+
+
+def highway_batch(key, messages, width: int = 64, rounds: int = 4,
+                  kernel: int = KERNEL_AUTO, out: Optional[torch.Tensor] = None):
+    """HighwayHash-64/128/256 of every row of an (n, L) uint8 batch."""
+    _check_width(width)
+    if rounds < 0:
+        raise ValueError("rounds must be >= 0")
+    return _fixed("hh", as_key256(key), messages, width, rounds, 0, width // 64, kernel, out)
+
+
+def sip_batch(key, messages, c: int = 2, d: int = 4, tree: bool = False,
+              kernel: int = KERNEL_AUTO, out: Optional[torch.Tensor] = None):
+    """SipHash-c-d (tree=False) or SipTreeHash (tree=True) of every row."""
+    if c < 1 or d < 1:
+        raise ValueError("round counts must be positive")
+    return _fixed("sip", as_key128(key), messages, c, d, int(bool(tree)), 1, kernel, out)
+
+
+# ---------------------------------------------------------------------------
+# Ragged batches
+# ---------------------------------------------------------------------------
+
+def _to_device(x, dtype, device):
+    if isinstance(x, torch.Tensor):
+        if x.dtype != dtype:
+            raise ValueError(f"expected {dtype}, got {x.dtype}")
+        return x.to(device, non_blocking=True).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x).view(
+        {torch.uint8: np.uint8, torch.int64: np.int64, torch.int32: np.int32}[dtype])
+    ).to(device).contiguous()
+
+
+def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None):
+    device = _require_cuda()
+    host = not (isinstance(buf, torch.Tensor) and buf.is_cuda)
+    if isinstance(offsets, np.ndarray):
+        offsets = offsets.astype(np.uint64, copy=False).view(np.int64)
+    if isinstance(lengths, np.ndarray):
+        lengths = lengths.astype(np.uint32, copy=False).view(np.int32)
+    if isinstance(buf, np.ndarray):
+        buf = buf.astype(np.uint8, copy=False).reshape(-1)
+    d_buf = _to_device(buf, torch.uint8, device)
+    d_off = _to_device(offsets, torch.int64, device)
+    d_len = None if lengths is None else _to_device(lengths, torch.int32, device)
+    n = d_off.numel() - 1 if d_len is None else d_off.numel()
+    if d_len is not None and d_len.numel() != n:
+        raise ValueError("offsets and lengths disagree on the message count")
+    if n < 0:
+        raise ValueError("offsets must hold n+1 entries when lengths is None")
+    if out is None:
+        out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=device)
+    if n:
+        st = _stream_ptr(device)
+        bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
+        lp = d_len.data_ptr() if d_len is not None else None
+        if kind == "hh":
+            rc = _lib.lib().lh_highway_ragged(bp, d_off.data_ptr(), lp, n, _key4(key), p1, p2,
+                                              out.data_ptr(), st)
+        else:
+            rc = _lib.lib().lh_siphash_ragged(bp, d_off.data_ptr(), lp, n, _key2(key), p1, p2,
+                                              tree, out.data_ptr(), st)
+        _lib.check(rc, "ragged batch")
+    if host:
+        return to_u64(out)
+    return out
+
+
+def highway_ragged(key, buf, offsets, lengths=None, width: int = 64, rounds: int = 4,
+                   out: Optional[torch.Tensor] = None):
+    """HighwayHash over a packed ragged buffer.  Message i is
+    buf[offsets[i] : offsets[i] + len_i] with len_i = lengths[i] when given,
+    else offsets[i+1] - offsets[i] (offsets then holds n+1 entries)."""
+    _check_width(width)
+    if rounds < 0:
+        raise ValueError("rounds must be >= 0")
+    return _ragged("hh", as_key256(key), buf, offsets, lengths, width, rounds, 0,
+                   width // 64, out)
+
+
+def sip_ragged(key, buf, offsets, lengths=None, c: int = 2, d: int = 4, tree: bool = False,
+               out: Optional[torch.Tensor] = None):
+    if c < 1 or d < 1:
+        raise ValueError("round counts must be positive")
+    return _ragged("sip", as_key128(key), buf, offsets, lengths, c, d, int(bool(tree)), 1, out)
+
+
+# ---------------------------------------------------------------------------
+# PRF mode and one-shot helpers
+# ---------------------------------------------------------------------------
+
+def prf64(key, start: int, n: int, rounds: int = 4, out: Optional[torch.Tensor] = None):
+    """out[i] = HighwayHash-64(key, le64(start + i)) for i < n (device tensor)."""
+    device = _require_cuda()
+    if n < 0 or rounds < 0:
+        raise ValueError("n and rounds must be >= 0")
+    if out is None:
+        out = torch.empty((n,), dtype=torch.int64, device=device)
+    if n:
+        rc = _lib.lib().lh_highway_prf64(start, n, _key4(as_key256(key)), rounds,
+                                         out.data_ptr(), _stream_ptr(device))
+        _lib.check(rc, "lh_highway_prf64")
+    return out
+
+
+def _one(message) -> torch.Tensor:
+    device = _require_cuda()
+    raw = bytes(message)
+    t = torch.frombuffer(bytearray(raw or b"\0"), dtype=torch.uint8)
+    return t.to(device)[: len(raw)].reshape(1, len(raw)), device
+
+
+def hash_one(key: Key256, message, width: int, rounds: int) -> np.ndarray:
+    _check_width(width)
+    if rounds < 0:
+        raise ValueError("rounds must be >= 0")
+    m, device = _one(message)
+    out = torch.empty((width // 64,), dtype=torch.int64, device=device)
+    _launch_fixed("hh", key, m, 1, m.shape[1], width, rounds, 0, out, KERNEL_AUTO, device)
+    return to_u64(out)
+
+
+def sip_one(key: Key128, message, c: int, d: int, tree: bool) -> int:
+    if c < 1 or d < 1:
+        raise ValueError("round counts must be positive")
+    m, device = _one(message)
+    out = torch.empty((1,), dtype=torch.int64, device=device)
+    _launch_fixed("sip", key, m, 1, m.shape[1], c, d, int(bool(tree)), out, KERNEL_AUTO, device)
+    return int(to_u64(out)[0])

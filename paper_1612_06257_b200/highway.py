@@ -1,0 +1,122 @@
+"""HighwayHash types and one-shot API, computed on the B200 engine.
+
+Mirrors the reference module ``lanehash.highway`` (S/highway.py): the same
+``Key256`` type, constants, digest byte images and ``hash64`` / ``hash256``
+signatures (S/highway.py:43-70, 20-38, 247-254, 288-295), plus ``hash128``
+(lanes 0-1 of the 256-bit lane sum; the reference defines no 128-bit width,
+S/highway.py:228-229 — derived).  Every digest is computed by
+the CUDA library; there is no Python arithmetic path.
+"""
+from __future__ import annotations
+
+import struct
+from typing import Iterable, Sequence, Tuple
+
+_MASK64 = 0xFFFFFFFFFFFFFFFF
+
+#: S/highway.py:20-31 (lane 0 first).  The engine carries its own copy in
+#: csrc/lh_engine.cu; tests/test_host.py checks both against the reference.
+INIT0: Tuple[int, int, int, int] = (
+    0xDBE6D5D5FE4CCE2F,
+    0xA4093822299F31D0,
+    0x13198A2E03707344,
+    0x243F6A8885A308D3,
+)
+INIT1: Tuple[int, int, int, int] = (
+    0x3BD39E10CB0EF593,
+    0xC0ACF169B5F18A8C,
+    0xBE5466CF34E90C6C,
+    0x452821E638D01377,
+)
+#: S/highway.py:35-38; realised on the GPU as 6 PRMT per lane pair
+#: (csrc/lh_device.cuh: zipper).
+ZIPPER_OFFSETS: Tuple[int, ...] = (
+    0x3, 0xC, 0x2, 0x5, 0xE, 0x1, 0xF, 0x0,
+    0xB, 0x4, 0xA, 0xD, 0x9, 0x6, 0x8, 0x7,
+)
+
+WIDTHS = (64, 128, 256)
+
+
+class Key256:
+    """256-bit key held as four 64-bit little-endian lanes (S/highway.py:43-70)."""
+
+    __slots__ = ("lanes",)
+
+    def __init__(self, lanes: Sequence[int]):
+        if len(lanes) != 4:
+            raise ValueError("Key256 requires exactly 4 lanes")
+        self.lanes = tuple(int(lane) & _MASK64 for lane in lanes)
+
+    @classmethod
+    def from_bytes(cls, raw: bytes) -> "Key256":
+        if len(raw) != 32:
+            raise ValueError("Key256 requires exactly 32 bytes")
+        return cls(struct.unpack("<4Q", raw))
+
+    @classmethod
+    def from_hex(cls, text: str) -> "Key256":
+        return cls.from_bytes(bytes.fromhex(text))
+
+    def to_bytes(self) -> bytes:
+        return struct.pack("<4Q", *self.lanes)
+
+    def __eq__(self, other: object) -> bool:
+        return isinstance(other, Key256) and self.lanes == other.lanes
+
+    def __hash__(self) -> int:
+        return hash(self.lanes)
+
+    def __repr__(self) -> str:
+        return f"Key256({self.to_bytes().hex()})"
+
+
+def as_key256(key) -> Key256:
+    """Accept a Key256, 32 raw bytes, or 4 integer lanes (numpy array ok)."""
+    if isinstance(key, Key256):
+        return key
+    if isinstance(key, (bytes, bytearray, memoryview)):
+        return Key256.from_bytes(bytes(key))
+    return Key256([int(x) for x in key])
+
+
+def _check_width(width: int) -> None:
+    if width not in WIDTHS:
+        raise ValueError("width must be 64, 128 or 256")
+
+
+def hash64(key, message: bytes, rounds: int = 4) -> int:
+    """One-shot 64-bit HighwayHash (S/highway.py:247-249) on the GPU."""
+    from . import engine
+
+    return int(engine.hash_one(as_key256(key), message, 64, rounds)[0])
+
+
+def hash128(key, message: bytes, rounds: int = 4) -> Tuple[int, int]:
+    """One-shot 128-bit HighwayHash: lanes 0-1 of the 256-bit lane sum."""
+    from . import engine
+
+    out = engine.hash_one(as_key256(key), message, 128, rounds)
+    return (int(out[0]), int(out[1]))
+
+
+def hash256(key, message: bytes, rounds: int = 4) -> Tuple[int, int, int, int]:
+    """One-shot 256-bit HighwayHash as four lanes (S/highway.py:252-254)."""
+    from . import engine
+
+    out = engine.hash_one(as_key256(key), message, 256, rounds)
+    return tuple(int(x) for x in out)
+
+
+def digest64_to_bytes(digest: int) -> bytes:
+    """Little-endian byte image of a 64-bit digest (S/highway.py:288-290)."""
+    return struct.pack("<Q", digest & _MASK64)
+
+
+def digest128_to_bytes(digest: Iterable[int]) -> bytes:
+    return struct.pack("<2Q", *(lane & _MASK64 for lane in digest))
+
+
+def digest256_to_bytes(digest: Iterable[int]) -> bytes:
+    """Lane 0 first, each lane little-endian (S/highway.py:293-295)."""
+    return struct.pack("<4Q", *(lane & _MASK64 for lane in digest))

@@ -1,0 +1,152 @@
+"""Host-side logic that runs without a GPU: the C-ABI library loads and exports
+every symbol include/lanehash_b200.h declares, argument validation and
+error mapping mirror the reference (ValueError), the reference-shaped types,
+and the synthetic-input generator's numpy twin."""
+import ctypes
+import struct
+
+import numpy as np
+import pytest
+
+import paper_1612_06257_b200 as lh
+from paper_1612_06257_b200 import _lib, engine, synth
+from paper_1612_06257_b200.highway import Key256
+from paper_1612_06257_b200.sip import Key128, SipParams
+
+
+def test_library_exports_every_declared_symbol():
+    l = _lib.lib()
+    declared = _lib.declared_symbols()
+    assert len(declared) >= 11
+    for name in declared:
+        assert hasattr(l, name), name
+
+
+def test_version_and_strerror():
+    assert "sm_100a" in _lib.version()
+    l = _lib.lib()
+    for code in (0, -1, -2, -3, -4, -5, -99):
+        assert l.lh_strerror(code)
+
+
+def test_abi_rejects_bad_arguments_before_touching_the_device():
+    l = _lib.lib()
+    key4 = (ctypes.c_uint64 * 4)(1, 2, 3, 4)
+    key2 = (ctypes.c_uint64 * 2)(1, 2)
+    buf = ctypes.create_string_buffer(64)
+    out = (ctypes.c_uint64 * 8)()
+    addr = ctypes.addressof
+    # width not in {64,128,256}
+    assert l.lh_highway_fixed(addr(buf), 1, 32, key4, 96, 4, addr(out), None) == _lib.LH_EINVAL
+    # negative rounds
+    assert l.lh_highway_fixed(addr(buf), 1, 32, key4, 64, -1, addr(out), None) == _lib.LH_EINVAL
+    # NULL key / NULL out
+    assert l.lh_highway_fixed(addr(buf), 1, 32, None, 64, 4, addr(out), None) == _lib.LH_EINVAL
+    assert l.lh_highway_fixed(addr(buf), 1, 32, key4, 64, 4, None, None) == _lib.LH_EINVAL
+    # misaligned digest pointer
+    assert l.lh_highway_fixed(addr(buf), 1, 32, key4, 64, 4, addr(out) + 1, None) == _lib.LH_EALIGN
+    # SipParams must be positive (S/sip.py:60-62)
+    assert l.lh_siphash_fixed(addr(buf), 1, 8, key2, 0, 4, 0, addr(out), None) == _lib.LH_EINVAL
+    assert l.lh_siphash_fixed(addr(buf), 1, 8, key2, 2, 0, 0, addr(out), None) == _lib.LH_EINVAL
+    # ragged: misaligned offsets
+    assert l.lh_highway_ragged(addr(buf), addr(buf) + 4, None, 1, key4, 64, 4, addr(out),
+                               None) == _lib.LH_EALIGN
+    # unknown kernel id
+    assert l.lh_highway_fixed_kernel(addr(buf), 1, 32, key4, 64, 4, addr(out), None, 7) == \
+        _lib.LH_EINVAL
+    # overflow of n * len
+    assert l.lh_highway_fixed(addr(buf), 1 << 40, 1 << 40, key4, 64, 4, addr(out), None) == \
+        _lib.LH_ETOOBIG
+    assert l.lh_synth_fill(addr(buf) + 1, 8, 0, 0, 0, None) == _lib.LH_EALIGN
+
+
+def test_check_maps_errors_like_the_reference():
+    with pytest.raises(ValueError):
+        _lib.check(_lib.LH_EINVAL)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.LH_EALIGN)
+    with pytest.raises(_lib.EngineError):
+        _lib.check(_lib.LH_ECUDA)
+    _lib.check(_lib.LH_OK)
+
+
+def test_python_api_validates_before_device():
+    with pytest.raises(ValueError):
+        engine.highway_batch(Key256((1, 2, 3, 4)), np.zeros((2, 32), np.uint8), width=96)
+    with pytest.raises(ValueError):
+        engine.sip_batch(Key128(1, 2), np.zeros((2, 32), np.uint8), c=0)
+    with pytest.raises(ValueError):
+        lh.select_backend("simd512")
+
+
+def test_constants_match_reference(golden):
+    assert [f"{x:016x}" for x in lh.INIT0] == golden["init0"]
+    assert [f"{x:016x}" for x in lh.INIT1] == golden["init1"]
+    assert list(lh.ZIPPER_OFFSETS) == golden["zipper_offsets"]
+    assert sorted(lh.ZIPPER_OFFSETS) == list(range(16))
+    assert bytes(lh.ZIPPER_OFFSETS).hex() == "030c02050e010f000b040a0d09060807"
+
+
+def test_zipper_prmt_selectors_match_byte_table():
+    """The GPU zipper (csrc/lh_device.cuh) is 6 PRMT per lane pair; replay the
+    same selectors with a Python byte_perm and compare to the byte table."""
+
+    def byte_perm(x, y, s):
+        src = struct.pack("<II", x, y)
+        return int.from_bytes(bytes(src[(s >> (4 * i)) & 7] for i in range(4)), "little")
+
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        data = rng.integers(0, 256, 16, dtype=np.uint8).tobytes()
+        w0, w1, w2, w3 = struct.unpack("<4I", data)
+        r0 = byte_perm(byte_perm(w0, w3, 0x0243), w1, 0x5210)
+        r1 = byte_perm(w3, w0, 0x4352)
+        r2 = byte_perm(byte_perm(w2, w1, 0x0243), w3, 0x5210)
+        r3 = byte_perm(w2, w1, 0x7061)
+        assert struct.pack("<4I", r0, r1, r2, r3) == bytes(data[o] for o in lh.ZIPPER_OFFSETS)
+
+
+def test_key_types_mirror_reference():
+    raw = bytes(range(32))
+    assert Key256.from_bytes(raw).to_bytes() == raw
+    assert Key256.from_hex(raw.hex()) == Key256.from_bytes(raw)
+    with pytest.raises(ValueError):
+        Key256.from_bytes(bytes(31))
+    with pytest.raises(ValueError):
+        Key256((1, 2, 3))
+    raw16 = bytes(range(16))
+    assert Key128.from_bytes(raw16).to_bytes() == raw16
+    with pytest.raises(ValueError):
+        Key128.from_bytes(bytes(8))
+    with pytest.raises(ValueError):
+        SipParams(0, 4)
+    with pytest.raises(ValueError):
+        SipParams(2, 0)
+
+
+def test_digest_byte_images():
+    assert lh.digest64_to_bytes(0x0102030405060708) == bytes((8, 7, 6, 5, 4, 3, 2, 1))
+    assert struct.unpack("<4Q", lh.digest256_to_bytes((1, 2, 3, 4))) == (1, 2, 3, 4)
+    assert struct.unpack("<2Q", lh.digest128_to_bytes((5, 6))) == (5, 6)
+
+
+def test_synth_numpy_twin_properties():
+    w = synth.words(1, 0, 1000)
+    assert len(np.unique(w)) == 1000
+    # word_offset windows agree
+    assert np.array_equal(synth.words(1, 500, 100), w[500:600])
+    b = synth.counter_bytes(1, 8 * 1000)
+    assert np.array_equal(b.view(np.uint64), w)
+    assert np.array_equal(synth.counter_bytes(1, 13), b[:13])
+    lens = synth.lengths(3, 100000, 8, 64)
+    assert lens.min() == 8 and lens.max() == 64
+    assert abs(lens.mean() - 36) < 0.2
+    k = synth.key256()
+    assert [f"{int(x):016x}" for x in k] == ["a30febcfd9c2825f", "4510bdf882d9d721",
+                                            "0a7d3da94ecde8b8", "043b27b61342f01d"]
+
+
+def test_remainder_sweep_layout():
+    lens, off, kind = synth.remainder_sweep_layout(1024, 64)
+    assert len(lens) == 65536 and int(off[-1]) == 33521664
+    assert (kind == 0).sum() == 32768 and (kind == 1).sum() == 16384
