@@ -235,8 +235,9 @@ def run_ours(args):
     total_ms_max = float(t.item())
 
     # checksum of checksums (validation only, outside the timed region)
-    fold = torch.tensor([int(np.bitwise_xor.reduce(engine.to_u64(out)))], dtype=torch.int64,
-                        device=dev)
+    fold_u = np.bitwise_xor.reduce(engine.to_u64(out))
+    fold = torch.tensor([int(np.array([fold_u], np.uint64).view(np.int64)[0])],
+                        dtype=torch.int64, device=dev)
     folds = [fold.clone() for _ in range(ws)]
     if ws > 1:
         dist.all_gather(folds, fold)

@@ -29,8 +29,12 @@ __device__ __forceinline__ u64 rot32(u64 x) { return pack(hi32(x), lo32(x)); }
 
 // mul32 (S/highway.py:80-82): low32(a) * high32(b), full 64-bit product.
 // One IMAD.WIDE.U32.
+// Written as PTX mul.wide.u32: the C++ form (u64)x * (u64)y made ptxas add a
+// zero high cross-term (an extra VIADD per multiply).
 __device__ __forceinline__ u64 mul_lo_hi(u64 a, u64 b) {
-  return (u64)lo32(a) * (u64)hi32(b);
+  u64 r;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(lo32(a)), "r"(hi32(b)));
+  return r;
 }
 
 // Zipper merge of one lane pair (S/highway.py:35-38, 73-77).  Output byte i

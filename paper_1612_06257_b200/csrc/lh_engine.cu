@@ -261,6 +261,11 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   // ---- consumers: thread t owns message row tile*ROWS + t ----
   const u32 t = threadIdx.x;
   const u32 sw = t & 7;
+  // Shared addresses of this thread's 8 swizzled 16-byte units in stage 0.
+  const u32 row0 = smem_u32(smem) + t * kBoxBytes;
+  u32 ua[8];
+#pragma unroll
+  for (u32 u = 0; u < 8; ++u) ua[u] = row0 + ((u ^ sw) << 4);
   const int W = nout(proto);
   const u64 nfull = len >> 5;
   const u32 r = (u32)(len & 31);  // 0 or 16
@@ -271,26 +276,27 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
     for (u32 c = 0; c < nchunks; ++c, ++it) {
       const u32 s = it % STAGES, ph = (it / STAGES) & 1;
       mbar_wait(&full_bar[s], ph);
-      const uint8_t* row = smem + s * kStageBytes + t * kBoxBytes;
+      const u32 so = s * kStageBytes;
       const u64 left = nfull - (u64)c * 4;
       const u32 kvalid = left >= 4 ? 4u : (u32)left;
       if (kvalid == 4) {
 #pragma unroll
         for (u32 k = 0; k < 4; ++k) {
-          const uint4 a = lds128(row + (((2 * k) ^ sw) << 4));
-          const uint4 b = lds128(row + (((2 * k + 1) ^ sw) << 4));
+          const uint4 a = lds128(ua[2 * k] + so);
+          const uint4 b = lds128(ua[2 * k + 1] + so);
           const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
           h.absorb32(p);
         }
       } else {
+        const u32 rowa = row0 + so;
         for (u32 k = 0; k < kvalid; ++k) {
-          const uint4 a = lds128(row + (((2 * k) ^ sw) << 4));
-          const uint4 b = lds128(row + (((2 * k + 1) ^ sw) << 4));
+          const uint4 a = lds128(rowa + (((2 * k) ^ sw) << 4));
+          const uint4 b = lds128(rowa + (((2 * k + 1) ^ sw) << 4));
           const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
           h.absorb32(p);
         }
         if (r) {
-          const uint4 a = lds128(row + (((2 * kvalid) ^ sw) << 4));
+          const uint4 a = lds128(rowa + (((2 * kvalid) ^ sw) << 4));
           tl[0] = pack(a.x, a.y);
           tl[1] = pack(a.z, a.w);
         }

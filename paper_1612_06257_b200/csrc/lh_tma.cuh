@@ -57,8 +57,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// Plain C++ shared load: ordered after mbar_wait by its "memory" clobber,
-// otherwise free for the compiler to schedule.
-__device__ __forceinline__ uint4 lds128(const void* p) { return *(const uint4*)p; }
+// 16-byte shared load from a 32-bit shared-window address (LDS.128).  Volatile
+// so it stays ordered after mbar_wait; the hash arithmetic still schedules
+// freely around it.
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(saddr));
+  return v;
+}
 
 }  // namespace lh
