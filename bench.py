@@ -252,7 +252,7 @@ def run_ours(args):
             "frac": round(achieved / peak, 4), "traffic": _traffic(),
             "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
-            "kernel": "k_tma_fixed<Highway,128,4,3>"}
+            "kernel": "k_tma_fixed<Highway,512,3,1>"}
     intp = _int_peak()
     if intp and intp.get("ops_per_s"):
         ops = (80 * (L // 32 + 4) + 4) * n

@@ -37,17 +37,34 @@ __device__ __forceinline__ u64 mul_lo_hi(u64 a, u64 b) {
   return r;
 }
 
+// 64-bit add split across the two integer pipes: low word IADD3 (ALU pipe,
+// carry out), high word IMAD.X hi*one + hi + carry (FMA pipe).  `one` is a
+// runtime 1 supplied by the host so ptxas cannot fold the IMAD back into an
+// ALU IADD3.X.  HighwayHash is ALU-pipe bound (PRMT, LOP3, IADD3 all issue
+// there); this moves the high halves of all 20 64-bit adds per Update to the FMA
+// pipe (ALU: 20 PRMT + 16 LOP3 + 20 IADD3 = 56; FMA: 8 IMAD.WIDE + 20 IMAD.X).
+__device__ __forceinline__ u64 add64_mixed(u64 a, u64 b, u32 one) {
+  u32 lo, hi;
+  asm("add.cc.u32 %0, %2, %3;\n\t"
+      "madc.lo.u32 %1, %4, %6, %5;"
+      : "=r"(lo), "=r"(hi)
+      : "r"(lo32(a)), "r"(lo32(b)), "r"(hi32(a)), "r"(hi32(b)), "r"(one));
+  return pack(lo, hi);
+}
+
 // Zipper merge of one lane pair (S/highway.py:35-38, 73-77).  Output byte i
 // of the 16-byte pair comes from input byte ZIP[i] = 3 C 2 5 E 1 F 0 B 4 A D
 // 9 6 8 7.  With input words W0..W3 (bytes 0-3, 4-7, 8-11, 12-15):
 //   R0 = [b3 b12 b2 b5]   R1 = [b14 b1 b15 b0]
 //   R2 = [b11 b4 b10 b13] R3 = [b9 b6 b8 b7]
-// which is 6 PRMT per pair.
+// R0 and R2 each draw on three input words; both take their W1/W3 bytes from
+// one shared intermediate u = [b5 b12 b4 b13], so the pair costs 5 PRMT.
 __device__ __forceinline__ void zipper(u64 lo, u64 hi, u64& zlo, u64& zhi) {
   const u32 w0 = lo32(lo), w1 = hi32(lo), w2 = lo32(hi), w3 = hi32(hi);
-  const u32 r0 = __byte_perm(__byte_perm(w0, w3, 0x0243), w1, 0x5210);
+  const u32 u = __byte_perm(w1, w3, 0x5041);
+  const u32 r0 = __byte_perm(w0, u, 0x4253);
   const u32 r1 = __byte_perm(w3, w0, 0x4352);
-  const u32 r2 = __byte_perm(__byte_perm(w2, w1, 0x0243), w3, 0x5210);
+  const u32 r2 = __byte_perm(w2, u, 0x7263);
   const u32 r3 = __byte_perm(w2, w1, 0x7061);
   zlo = pack(r0, r1);
   zhi = pack(r2, r3);
@@ -63,6 +80,7 @@ struct Highway {
   u64 v0[4], v1[4], m0[4], m1[4];
   int rounds;
   int width;  // 64, 128 or 256
+  u32 one;    // = 1, opaque to the compiler (see add64_mixed)
 
   __device__ __forceinline__ void init(const HHState& k, int rounds_, int width_) {
 #pragma unroll
@@ -82,24 +100,24 @@ struct Highway {
     const u64 p[4] = {p0, p1, p2, p3};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      v1[i] += p[i] + m0[i];
+      v1[i] = add64_mixed(v1[i], add64_mixed(p[i], m0[i], one), one);
       m0[i] ^= mul_lo_hi(v1[i], v0[i]);
-      v0[i] += m1[i];
+      v0[i] = add64_mixed(v0[i], m1[i], one);
       m1[i] ^= mul_lo_hi(v0[i], v1[i]);
     }
     u64 z0, z1, z2, z3;
     zipper(v1[0], v1[1], z0, z1);
     zipper(v1[2], v1[3], z2, z3);
-    v0[0] += z0;
-    v0[1] += z1;
-    v0[2] += z2;
-    v0[3] += z3;
+    v0[0] = add64_mixed(v0[0], z0, one);
+    v0[1] = add64_mixed(v0[1], z1, one);
+    v0[2] = add64_mixed(v0[2], z2, one);
+    v0[3] = add64_mixed(v0[3], z3, one);
     zipper(v0[0], v0[1], z0, z1);
     zipper(v0[2], v0[3], z2, z3);
-    v1[0] += z0;
-    v1[1] += z1;
-    v1[2] += z2;
-    v1[3] += z3;
+    v1[0] = add64_mixed(v1[0], z0, one);
+    v1[1] = add64_mixed(v1[1], z1, one);
+    v1[2] = add64_mixed(v1[2], z2, one);
+    v1[3] = add64_mixed(v1[3], z3, one);
   }
 
   __device__ __forceinline__ void absorb32(const u64 (&p)[4]) {

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/lanehash_b200.h"
@@ -52,6 +53,7 @@ Highway make_highway(const u64 key[4], int width, int rounds) {
   }
   h.rounds = rounds;
   h.width = width;
+  h.one = 1;
   return h;
 }
 
@@ -218,11 +220,13 @@ constexpr size_t tma_smem_bytes() {
 template <class H, int ROWS, int STAGES, int MINB>
 __global__ void __launch_bounds__(ROWS + 32, MINB)
     k_tma_fixed(const __grid_constant__ CUtensorMap tmap, const H proto, u64 n, u64 len,
-                u64* __restrict__ out) {
+                u64* __restrict__ out, u32 pf) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr u32 kStageBytes = ROWS * kBoxBytes;
   constexpr int kConsumerWarps = ROWS / 32;
+  constexpr int kBoxRowsTma = ROWS < 256 ? ROWS : 256;  // TMA box rows <= 256
+  constexpr int kBoxesPerStage = ROWS / kBoxRowsTma;
   uint64_t* full_bar = (uint64_t*)(smem + STAGES * kStageBytes);
   uint64_t* empty_bar = full_bar + STAGES;
 
@@ -244,14 +248,33 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
     // ---- producer: one elected lane streams boxes into the ring ----
     if (lane == 0) {
       tma_prefetch_desc(&tmap);
+      // L2 prefetch cursor, `pf` boxes ahead of the loads: the ring is only
+      // STAGES deep, so the loads themselves would expose DRAM latency.
+      u64 pf_tile = blockIdx.x;
+      u32 pf_c = 0;
+      for (u32 k = 0; k < pf && pf_tile < ntiles; ++k) {
+        for (int b = 0; b < kBoxesPerStage; ++b)
+          tma_prefetch_l2_2d(&tmap, (int32_t)(pf_c * kBoxBytes),
+                             (int32_t)(pf_tile * ROWS + b * kBoxRowsTma));
+        if (++pf_c == nchunks) { pf_c = 0; pf_tile += gridDim.x; }
+      }
       u32 it = 0;
       for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (u32 c = 0; c < nchunks; ++c, ++it) {
           const u32 s = it % STAGES, ph = (it / STAGES) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
           mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-          tma_load_2d(smem + s * kStageBytes, &tmap, (int32_t)(c * kBoxBytes),
-                      (int32_t)(tile * ROWS), &full_bar[s]);
+#pragma unroll
+          for (int b = 0; b < kBoxesPerStage; ++b)
+            tma_load_2d(smem + s * kStageBytes + b * kBoxRowsTma * kBoxBytes, &tmap,
+                        (int32_t)(c * kBoxBytes), (int32_t)(tile * ROWS + b * kBoxRowsTma),
+                        &full_bar[s]);
+          if (pf && pf_tile < ntiles) {
+            for (int b = 0; b < kBoxesPerStage; ++b)
+              tma_prefetch_l2_2d(&tmap, (int32_t)(pf_c * kBoxBytes),
+                                 (int32_t)(pf_tile * ROWS + b * kBoxRowsTma));
+            if (++pf_c == nchunks) { pf_c = 0; pf_tile += gridDim.x; }
+          }
         }
       }
     }
@@ -350,6 +373,16 @@ unsigned grid_for(u64 n, int threads, int sms) {
   return (unsigned)(blocks < cap ? (blocks ? blocks : 1) : cap);
 }
 
+u32 tma_l2_prefetch() {
+  static int pf = -1;
+  if (pf < 0) {
+    const char* s = getenv("LH_TMA_PF");
+    pf = s ? atoi(s) : 0;
+    if (pf < 0) pf = 0;
+  }
+  return (u32)pf;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -398,7 +431,7 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)len, (cuuint64_t)nn};
     cuuint64_t strides[1] = {(cuuint64_t)len};
-    cuuint32_t box[2] = {(cuuint32_t)kBoxBytes, (cuuint32_t)ROWS};
+    cuuint32_t box[2] = {(cuuint32_t)kBoxBytes, (cuuint32_t)(ROWS < 256 ? ROWS : 256)};
     cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)(msgs + base * len), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -408,11 +441,28 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
     const u64 tiles = (nn + ROWS - 1) / ROWS;
     const u64 cap = (u64)sms * per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    kern<<<grid, ROWS + 32, smem, st>>>(map, proto, nn, len, out + base * W);
+    kern<<<grid, ROWS + 32, smem, st>>>(map, proto, nn, len, out + base * W, tma_l2_prefetch());
     int rc = cuda_err(cudaGetLastError());
     if (rc) return rc;
   }
   return LH_OK;
+}
+
+// Tuning knobs (read once): LH_TMA_CFG=128x4|256x3|512x3|128x3 tile shape,
+// LH_TMA_PF=<boxes> L2 prefetch distance.  Defaults: automatic.
+int tma_cfg_override() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* s = getenv("LH_TMA_CFG");
+    cfg = 0;
+    if (s) {
+      if (!strcmp(s, "128x4")) cfg = 1;
+      else if (!strcmp(s, "256x3")) cfg = 2;
+      else if (!strcmp(s, "512x3")) cfg = 3;
+      else if (!strcmp(s, "128x3")) cfg = 4;
+    }
+  }
+  return cfg;
 }
 
 template <class H>
@@ -421,9 +471,21 @@ int launch_tma(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out, cu
   int rc = check_device(&sms);
   if (rc) return rc;
   if (n == 0) return LH_OK;
-  // Long messages with few rows: 32-row tiles keep more SMs busy.
-  if (n < (u64)sms * 3 * 128) return launch_tma_cfg<H, 32, 8, 4>(proto, msgs, n, len, out, st, sms);
-  return launch_tma_cfg<H, 128, 4, 3>(proto, msgs, n, len, out, st, sms);
+  switch (tma_cfg_override()) {
+    case 1: return launch_tma_cfg<H, 128, 4, 3>(proto, msgs, n, len, out, st, sms);
+    case 2: return launch_tma_cfg<H, 256, 3, 2>(proto, msgs, n, len, out, st, sms);
+    case 3: return launch_tma_cfg<H, 512, 3, 1>(proto, msgs, n, len, out, st, sms);
+    case 4: return launch_tma_cfg<H, 128, 3, 4>(proto, msgs, n, len, out, st, sms);
+    default: break;
+  }
+  // One 512-row CTA per SM (16 consumer warps sharing a 3 x 64 KiB ring)
+  // measured fastest for large batches (profiles/README.md); smaller batches
+  // use smaller tiles so every SM gets several, and few-but-long messages
+  // use 32-row tiles to spread over as many SMs as possible.
+  if (n >= (u64)sms * 512 * 8) return launch_tma_cfg<H, 512, 3, 1>(proto, msgs, n, len, out, st, sms);
+  if (n >= (u64)sms * 128 * 3 * 4)
+    return launch_tma_cfg<H, 128, 4, 3>(proto, msgs, n, len, out, st, sms);
+  return launch_tma_cfg<H, 32, 8, 4>(proto, msgs, n, len, out, st, sms);
 }
 
 bool tma_ok(const uint8_t* msgs, u64 n, u64 len) {

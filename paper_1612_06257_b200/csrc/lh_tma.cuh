@@ -57,6 +57,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Bulk L2 prefetch of one 2-D box (no shared memory, no completion).
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((uint64_t)map),
+               "r"(x), "r"(y)
+               : "memory");
+}
+
 // 16-byte shared load from a 32-bit shared-window address (LDS.128).  Volatile
 // so it stays ordered after mbar_wait; the hash arithmetic still schedules
 // freely around it.

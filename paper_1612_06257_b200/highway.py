@@ -28,7 +28,7 @@ INIT1: Tuple[int, int, int, int] = (
     0xBE5466CF34E90C6C,
     0x452821E638D01377,
 )
-#: S/highway.py:35-38; realised on the GPU as 6 PRMT per lane pair
+#: S/highway.py:35-38; realised on the GPU as 5 PRMT per lane pair
 #: (csrc/lh_device.cuh: zipper).
 ZIPPER_OFFSETS: Tuple[int, ...] = (
     0x3, 0xC, 0x2, 0x5, 0xE, 0x1, 0xF, 0x0,

@@ -88,7 +88,7 @@ def test_constants_match_reference(golden):
 
 
 def test_zipper_prmt_selectors_match_byte_table():
-    """The GPU zipper (csrc/lh_device.cuh) is 6 PRMT per lane pair; replay the
+    """The GPU zipper (csrc/lh_device.cuh) is 5 PRMT per lane pair; replay the
     same selectors with a Python byte_perm and compare to the byte table."""
 
     def byte_perm(x, y, s):
@@ -99,9 +99,10 @@ def test_zipper_prmt_selectors_match_byte_table():
     for _ in range(200):
         data = rng.integers(0, 256, 16, dtype=np.uint8).tobytes()
         w0, w1, w2, w3 = struct.unpack("<4I", data)
-        r0 = byte_perm(byte_perm(w0, w3, 0x0243), w1, 0x5210)
+        u = byte_perm(w1, w3, 0x5041)
+        r0 = byte_perm(w0, u, 0x4253)
         r1 = byte_perm(w3, w0, 0x4352)
-        r2 = byte_perm(byte_perm(w2, w1, 0x0243), w3, 0x5210)
+        r2 = byte_perm(w2, u, 0x7263)
         r3 = byte_perm(w2, w1, 0x7061)
         assert struct.pack("<4I", r0, r1, r2, r3) == bytes(data[o] for o in lh.ZIPPER_OFFSETS)
 
