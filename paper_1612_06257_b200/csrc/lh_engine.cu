@@ -286,9 +286,12 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   const u32 sw = t & 7;
   // Shared addresses of this thread's 8 swizzled 16-byte units in stage 0.
   const u32 row0 = smem_u32(smem) + t * kBoxBytes;
+  // Kept live in registers (opaque to ptxas, which would otherwise recompute
+  // them per chunk); the stage offset is folded into LDS immediates below.
   u32 ua[8];
 #pragma unroll
-  for (u32 u = 0; u < 8; ++u) ua[u] = row0 + ((u ^ sw) << 4);
+  for (u32 u = 0; u < 8; ++u)
+    asm volatile("mov.b32 %0, %1;" : "=r"(ua[u]) : "r"(row0 + ((u ^ sw) << 4)));
   const int W = nout(proto);
   const u64 nfull = len >> 5;
   const u32 r = (u32)(len & 31);  // 0 or 16
@@ -303,12 +306,19 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
       const u64 left = nfull - (u64)c * 4;
       const u32 kvalid = left >= 4 ? 4u : (u32)left;
       if (kvalid == 4) {
+        // One copy of the 4-packet body per stage, so `so` is a compile-time
+        // LDS offset (no per-chunk address arithmetic on the ALU pipe).
 #pragma unroll
-        for (u32 k = 0; k < 4; ++k) {
-          const uint4 a = lds128(ua[2 * k] + so);
-          const uint4 b = lds128(ua[2 * k + 1] + so);
-          const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
-          h.absorb32(p);
+        for (u32 ss = 0; ss < (u32)STAGES; ++ss) {
+          if (s == ss) {
+#pragma unroll
+            for (u32 k = 0; k < 4; ++k) {
+              const uint4 a = lds128(ua[2 * k] + ss * kStageBytes);
+              const uint4 b = lds128(ua[2 * k + 1] + ss * kStageBytes);
+              const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
+              h.absorb32(p);
+            }
+          }
         }
       } else {
         const u32 rowa = row0 + so;
