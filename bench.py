@@ -80,7 +80,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period: float = 0.01):
+    def __init__(self, index: int, period: float = 0.05):
         self.samples, self.reasons, self.max_mhz = [], 0, None
         self.period, self._stop = period, threading.Event()
         self.ok = False
@@ -277,6 +277,9 @@ def run_ours(args):
                        "parallelism": f"dp{ws} (message-index shards, no collective)",
                        "l2": "inputs 16 GiB per GPU >> 126 MB L2; no flush needed"},
             "msgs_per_s": round(ws * n * args.steps / (total_ms_max / 1e3), 1),
+            "step_ms": {"min": round(float(np.min(step_ms)), 4),
+                        "median": round(float(np.median(step_ms)), 4),
+                        "max": round(float(np.max(step_ms)), 4)},
             "roofline": roof,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
