@@ -47,6 +47,8 @@ extern "C" {
 #define LH_KERNEL_AUTO 0
 #define LH_KERNEL_DIRECT 1 /* one thread per message, direct global loads */
 #define LH_KERNEL_TMA 2    /* TMA-staged shared-memory ring (fixed length) */
+#define LH_KERNEL_SPLIT 3  /* HighwayHash only: state split over 2 threads per
+                              message (long messages; len % 128 == 0) */
 
 /* Library / build identification. */
 const char* lh_version(void);

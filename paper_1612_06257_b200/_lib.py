@@ -25,6 +25,7 @@ LH_ETOOBIG = -5
 KERNEL_AUTO = 0
 KERNEL_DIRECT = 1
 KERNEL_TMA = 2
+KERNEL_SPLIT = 3
 
 _lib = None
 

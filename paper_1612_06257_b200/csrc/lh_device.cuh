@@ -174,6 +174,104 @@ struct Highway {
   }
 };
 
+// HighwayHash with the 1024-bit state split over a thread pair (long
+// messages, few of them).  Half h = 0 holds lanes {0,1}, h = 1 lanes {2,3}.
+// Update never mixes the halves (per-lane steps 1-5, zipper pairs (0,1) and
+// (2,3), S/highway.py:137-149), so it runs thread-locally on half the work;
+// only PermuteAndUpdate (S/highway.py:176-179) crosses halves: half 0's new
+// packet words are rot32 of half 1's v0 and vice versa — one 64-bit
+// __shfl_xor pair per word per round.  Partner = lane ^ 1.
+struct HighwayHalf {
+  u64 v0[2], v1[2], m0[2], m1[2];
+  int rounds;
+  int width;
+  u32 one;
+  u32 half;
+
+  __device__ __forceinline__ void init(const Highway& full, u32 h) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      v0[i] = h ? full.v0[2 + i] : full.v0[i];
+      v1[i] = h ? full.v1[2 + i] : full.v1[i];
+      m0[i] = h ? full.m0[2 + i] : full.m0[i];
+      m1[i] = h ? full.m1[2 + i] : full.m1[i];
+    }
+    rounds = full.rounds;
+    width = full.width;
+    one = full.one;
+    half = h;
+  }
+
+  __device__ __forceinline__ void update(u64 pa, u64 pb) {
+    const u64 p[2] = {pa, pb};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      v1[i] = add64_mixed(v1[i], add64_mixed(p[i], m0[i], one), one);
+      m0[i] ^= mul_lo_hi(v1[i], v0[i]);
+      v0[i] = add64_mixed(v0[i], m1[i], one);
+      m1[i] ^= mul_lo_hi(v0[i], v1[i]);
+    }
+    u64 z0, z1;
+    zipper(v1[0], v1[1], z0, z1);
+    v0[0] = add64_mixed(v0[0], z0, one);
+    v0[1] = add64_mixed(v0[1], z1, one);
+    zipper(v0[0], v0[1], z0, z1);
+    v1[0] = add64_mixed(v1[0], z0, one);
+    v1[1] = add64_mixed(v1[1], z1, one);
+  }
+
+  // t: the full 32-byte tail (both threads hold it), r = len % 32.
+  __device__ __forceinline__ void remainder(const u64 (&t)[4], u32 r) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      v0[i] = pack(lo32(v0[i]) + r, hi32(v0[i]) + r);
+      v1[i] = pack(__funnelshift_l(lo32(v1[i]), lo32(v1[i]), r),
+                   __funnelshift_l(hi32(v1[i]), hi32(v1[i]), r));
+    }
+    const u32 whole = r & ~3u;
+    u64 p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int keep = (int)whole - 8 * k;
+      const u64 mask = keep >= 8 ? ~0ull : (keep <= 0 ? 0ull : ((1ull << (8 * keep)) - 1));
+      p[k] = t[k] & mask;
+    }
+    const u64 s01 = (whole & 8) ? t[1] : t[0];
+    const u64 s23 = (whole & 8) ? t[3] : t[2];
+    const u64 src = (whole & 16) ? s23 : s01;
+    u32 left = (whole & 4) ? hi32(src) : lo32(src);
+    const u32 nleft = r & 3u;
+    left &= nleft ? ((1u << (8 * nleft)) - 1u) : 0u;
+    p[3] |= (u64)left << 32;
+    update(half ? p[2] : p[0], half ? p[3] : p[1]);
+  }
+
+  __device__ __forceinline__ static u64 shfl_xor1(u64 x) {
+    return pack(__shfl_xor_sync(0xffffffffu, lo32(x), 1), __shfl_xor_sync(0xffffffffu, hi32(x), 1));
+  }
+
+  // All 32 lanes of the warp must call this together (shuffles).
+  __device__ __forceinline__ void finalize_rounds() {
+    for (int i = 0; i < rounds; ++i) {
+      const u64 o0 = shfl_xor1(v0[0]), o1 = shfl_xor1(v0[1]);
+      update(rot32(o0), rot32(o1));
+    }
+  }
+
+  // Writes this half's lanes of the width/64 lane sums (lane 0 first).
+  __device__ __forceinline__ void store(u64* out) const {
+    const u64 s0 = v0[0] + v1[0] + m0[0] + m1[0];
+    const u64 s1 = v0[1] + v1[1] + m0[1] + m1[1];
+    if (half == 0) {
+      out[0] = s0;
+      if (width >= 128) out[1] = s1;
+    } else if (width == 256) {
+      out[2] = s0;
+      out[3] = s1;
+    }
+  }
+};
+
 // ---------------- SipHash-c-d (S/sip.py:73-108) ----------------
 
 __device__ __forceinline__ u64 rotl64(u64 x, int b) {

@@ -343,6 +343,121 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
 }
 
 // --------------------------------------------------------------------------
+// Long-message kernel: the HighwayHash state of each message is split over a
+// thread pair (lh::HighwayHalf), so a batch of few long messages fills twice
+// as many warps (cfg4: 16,384 x 1 MiB = 1,024 warps instead of 512).
+// One warp per CTA = 16 messages.  Requirements: len % 128 == 0, 16-B
+// aligned base.  The byte matrix is viewed as a 3-D tensor
+// {128 B, n rows, len/128 chunks}; one TMA box = 16 rows x CH chunks
+// (16 x 512 B = 8 KiB for CH = 4), laid out [chunk][row][128 B] with the
+// 128-byte swizzle, into a STAGES-deep ring refilled by lane 0 as soon as
+// the warp has consumed a stage.  Half 0 of row r reads unit 2k of packet
+// k, half 1 unit 2k+1 (2-way bank conflict; shared memory is not the
+// limiter here).
+// --------------------------------------------------------------------------
+constexpr int kSplitRows = 16;
+
+template <int STAGES, int CH>
+constexpr size_t split_smem_bytes() {
+  return 1024 + (size_t)STAGES * kSplitRows * CH * kBoxBytes + STAGES * 8;
+}
+
+template <int STAGES, int CH, int MINB>
+__global__ void __launch_bounds__(32, MINB)
+    k_tma_split(const __grid_constant__ CUtensorMap tmap, const Highway proto, u64 n, u64 len,
+                u64* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr u32 kChunk = kSplitRows * kBoxBytes;  // 2 KiB: one 128-B chunk of 16 rows
+  constexpr u32 kStage = CH * kChunk;
+  uint64_t* bar = (uint64_t*)(smem + STAGES * kStage);
+  const u32 lane = threadIdx.x & 31, row = lane >> 1, half = lane & 1, sw = row & 7;
+
+  const u64 ntiles = (n + kSplitRows - 1) / kSplitRows;
+  const u32 nch = (u32)(len / kBoxBytes);
+  const u32 nst = (nch + CH - 1) / CH;  // stages per tile
+  const u64 g = blockIdx.x, G = gridDim.x;
+  const u64 my_tiles = g < ntiles ? (ntiles - g + G - 1) / G : 0;
+  const u64 total = my_tiles * nst;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmap);
+  }
+  __syncwarp();
+  u64 it_tile = g;
+  u32 it_st = 0;
+  auto issue_next = [&](u32 s) {
+    mbar_arrive_expect_tx(&bar[s], kStage);
+    tma_load_3d(smem + s * kStage, &tmap, 0, (int32_t)(it_tile * kSplitRows),
+                (int32_t)(it_st * CH), &bar[s]);
+    if (++it_st == nst) {
+      it_st = 0;
+      it_tile += G;
+    }
+  };
+  if (lane == 0)
+    for (u32 s = 0; s < (u32)STAGES && s < total; ++s) issue_next(s);
+
+  u32 ua[4];
+#pragma unroll
+  for (u32 k = 0; k < 4; ++k)
+    asm volatile("mov.b32 %0, %1;"
+                 : "=r"(ua[k])
+                 : "r"(smem_u32(smem) + row * kBoxBytes + (((2 * k + half) ^ sw) << 4)));
+
+  const int W = proto.width / 64;
+  HighwayHalf h;
+  h.init(proto, half);
+  u64 tile = g;
+  u32 st = 0, s = 0, ph = 0;
+  for (u64 i = 0; i < total; ++i) {
+    mbar_wait(&bar[s], ph);
+    const u32 nvalid = (nch - st * CH) < (u32)CH ? (nch - st * CH) : (u32)CH;
+    if (nvalid == (u32)CH) {
+#pragma unroll
+      for (u32 ss = 0; ss < (u32)STAGES; ++ss) {
+        if (s == ss) {
+#pragma unroll
+          for (u32 c = 0; c < (u32)CH; ++c)
+#pragma unroll
+            for (u32 k = 0; k < 4; ++k) {
+              const uint4 a = lds128(ua[k] + ss * kStage + c * kChunk);
+              h.update(pack(a.x, a.y), pack(a.z, a.w));
+            }
+        }
+      }
+    } else {
+      for (u32 c = 0; c < nvalid; ++c)
+#pragma unroll
+        for (u32 k = 0; k < 4; ++k) {
+          const uint4 a = lds128(ua[k] + s * kStage + c * kChunk);
+          h.update(pack(a.x, a.y), pack(a.z, a.w));
+        }
+    }
+    __syncwarp();
+    if (lane == 0 && i + STAGES < total) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_next(s);
+    }
+    if (++s == (u32)STAGES) {
+      s = 0;
+      ph ^= 1;
+    }
+    if (++st == nst) {
+      h.finalize_rounds();  // whole warp: shuffles between the halves
+      const u64 m = tile * kSplitRows + row;
+      if (m < n) h.store(out + m * W);
+      h.init(proto, half);
+      st = 0;
+      tile += G;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // PRF: hash64(key, le64(ctr)).  With r = 8 the remainder packet is
 // (ctr, 0, 0, 0) (S/highway.py:206-220) and the length injection is
 // key-only, so `proto` arrives already tweaked; per counter: 1 + rounds
@@ -458,6 +573,53 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
   return LH_OK;
 }
 
+int launch_split(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
+                 cudaStream_t st) {
+  constexpr int STAGES = 3, CH = 4, MINB = 8;
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  auto enc = get_encode();
+  if (!enc) return LH_ECUDA;
+  constexpr size_t smem = split_smem_bytes<STAGES, CH>();
+  auto kern = k_tma_split<STAGES, CH, MINB>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return LH_ECUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem) != cudaSuccess ||
+      per_sm < 1)
+    return LH_ECUDA;
+  const u64 kSeg = 1ull << 30;
+  const int W = proto.width / 64;
+  for (u64 base = 0; base < n; base += kSeg) {
+    const u64 nn = n - base < kSeg ? n - base : kSeg;
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)kBoxBytes, (cuuint64_t)nn, (cuuint64_t)(len / kBoxBytes)};
+    cuuint64_t strides[2] = {(cuuint64_t)len, (cuuint64_t)kBoxBytes};
+    cuuint32_t box[3] = {(cuuint32_t)kBoxBytes, (cuuint32_t)kSplitRows, (cuuint32_t)CH};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)(msgs + base * len), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return LH_ECUDA;
+    const u64 tiles = (nn + kSplitRows - 1) / kSplitRows;
+    const u64 cap = (u64)sms * per_sm;
+    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+    kern<<<grid, 32, smem, st>>>(map, proto, nn, len, out + base * W);
+    rc = cuda_err(cudaGetLastError());
+    if (rc) return rc;
+  }
+  return LH_OK;
+}
+
+bool split_ok(const uint8_t* msgs, u64 n, u64 len) {
+  return n > 0 && len >= 128 && len % 128 == 0 && ((uintptr_t)msgs % 16) == 0 &&
+         len / 128 < (1ull << 31);
+}
+
 // Tuning knobs (read once): LH_TMA_CFG=128x4|256x3|512x3|128x3 tile shape,
 // LH_TMA_PF=<boxes> L2 prefetch distance.  Defaults: automatic.
 int tma_cfg_override() {
@@ -504,8 +666,36 @@ bool tma_ok(const uint8_t* msgs, u64 n, u64 len) {
 }
 
 template <class H>
+int dispatch_split(const H&, const uint8_t*, u64, u64, u64*, cudaStream_t) {
+  return LH_EINVAL;  // only HighwayHash has a split-state kernel
+}
+template <>
+int dispatch_split<Highway>(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
+                            cudaStream_t st) {
+  if (!split_ok(msgs, n, len)) return LH_EINVAL;
+  return launch_split(proto, msgs, n, len, out, st);
+}
+
+template <class H>
+bool prefer_split(const H&, const uint8_t*, u64, u64) {
+  return false;
+}
+template <>
+bool prefer_split<Highway>(const Highway&, const uint8_t* msgs, u64 n, u64 len) {
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // Few long messages: one thread per message would leave SMs idle.
+  return split_ok(msgs, n, len) && len >= 4096 && n < (u64)sms * 256;
+}
+
+template <class H>
 int dispatch_fixed(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                    cudaStream_t st, int kernel) {
+  if (kernel == LH_KERNEL_SPLIT) return n ? dispatch_split(proto, msgs, n, len, out, st) : LH_OK;
+  if (kernel == LH_KERNEL_AUTO && prefer_split(proto, msgs, n, len))
+    return dispatch_split(proto, msgs, n, len, out, st);
   if (kernel == LH_KERNEL_TMA) {
     if (n && !tma_ok(msgs, n, len)) return LH_EINVAL;
     return launch_tma(proto, msgs, n, len, out, st);
@@ -550,7 +740,7 @@ int lh_highway_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
   if (!key || !valid_width(width) || rounds < 0 || (n && !d_out) || (n && len && !d_msgs))
     return LH_EINVAL;
   if ((uintptr_t)d_out % 8) return LH_EALIGN;
-  if (kernel < 0 || kernel > LH_KERNEL_TMA) return LH_EINVAL;
+  if (kernel < 0 || kernel > LH_KERNEL_SPLIT) return LH_EINVAL;
   if (len && n > UINT64_MAX / len) return LH_ETOOBIG;
   const Highway h = make_highway(key, width, rounds);
   return dispatch_fixed(h, d_msgs, n, len, d_out, (cudaStream_t)stream, kernel);

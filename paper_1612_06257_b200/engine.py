@@ -34,6 +34,7 @@ from .sip import Key128, as_key128
 KERNEL_AUTO = _lib.KERNEL_AUTO
 KERNEL_DIRECT = _lib.KERNEL_DIRECT
 KERNEL_TMA = _lib.KERNEL_TMA
+KERNEL_SPLIT = _lib.KERNEL_SPLIT
 
 #: Host-path chunk size (bytes of message payload per H2D copy).
 HOST_CHUNK_BYTES = 128 << 20

@@ -13,7 +13,7 @@ import torch
 
 from conftest import GOLDEN, golden_npy
 from paper_1612_06257_b200 import engine, synth
-from paper_1612_06257_b200.engine import KERNEL_DIRECT, KERNEL_TMA, to_u64
+from paper_1612_06257_b200.engine import KERNEL_DIRECT, KERNEL_SPLIT, KERNEL_TMA, to_u64
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 DEV = "cuda"
@@ -61,9 +61,11 @@ def test_cfg4_long_messages_16GiB(oracle, golden):
     n, L = 16384, 1 << 20
     buf = _fill(n * L, 5)
     m = buf.view(n, L)
-    a = engine.highway_batch(synth.key256(), m, 256, kernel=KERNEL_TMA)
+    a = engine.highway_batch(synth.key256(), m, 256)  # auto: split-state kernel
     b = engine.highway_batch(synth.key256(), m, 256, kernel=KERNEL_DIRECT)
-    assert torch.equal(a, b)
+    c = engine.highway_batch(synth.key256(), m, 256, kernel=KERNEL_TMA)
+    s = engine.highway_batch(synth.key256(), m, 256, kernel=KERNEL_SPLIT)
+    assert torch.equal(a, b) and torch.equal(a, c) and torch.equal(a, s)
     h = to_u64(a)
     assert [f"{int(x):016x}" for x in h[0]] == golden["cfg4_msg0_h256"]
     for i in (1, 777, n - 1):

@@ -16,7 +16,8 @@ import torch
 import paper_1612_06257_b200 as lh
 from conftest import golden_npy
 from paper_1612_06257_b200 import engine, synth
-from paper_1612_06257_b200.engine import KERNEL_AUTO, KERNEL_DIRECT, KERNEL_TMA, to_u64
+from paper_1612_06257_b200.engine import (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_SPLIT, KERNEL_TMA,
+                                          to_u64)
 from paper_1612_06257_b200.highway import Key256
 from paper_1612_06257_b200.sip import SIPHASH_13, SIPHASH_24, Key128, SipParams
 
@@ -276,3 +277,33 @@ def test_synth_device_matches_numpy():
     L = torch.empty(100000, dtype=torch.int32, device=DEV)
     synth.lengths_device(L, 3, 8, 64)
     assert np.array_equal(L.cpu().numpy().view(np.uint32), synth.lengths(3, 100000, 8, 64))
+
+
+# ---------------------------------------------------------------------------
+# split-state long-message kernel (2 threads per message)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,L", [(1, 128), (15, 256), (16, 640), (17, 1024), (300, 4096),
+                                 (33, 65536), (40, 128 * 37)])
+def test_split_kernel_vs_oracle(oracle, n, L):
+    key = synth.key256()
+    msgs = synth.counter_bytes(50 + n, n * L).reshape(n, L)
+    d = dev(msgs)
+    for width in (64, 128, 256):
+        want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, msgs, width, 4)
+        got = to_u64(engine.highway_batch(key, d, width, 4, kernel=KERNEL_SPLIT))
+        assert np.array_equal(got, want), (n, L, width)
+    for rounds in (0, 1, 5):
+        want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, msgs, 256, rounds)
+        got = to_u64(engine.highway_batch(key, d, 256, rounds, kernel=KERNEL_SPLIT))
+        assert np.array_equal(got, want), (n, L, rounds)
+
+
+def test_split_kernel_rejects_unsupported_shapes():
+    key = synth.key256()
+    with pytest.raises(ValueError):
+        engine.highway_batch(key, torch.zeros((4, 96), dtype=torch.uint8, device=DEV),
+                             kernel=KERNEL_SPLIT)
+    with pytest.raises(ValueError):
+        engine.sip_batch(synth.key128(), torch.zeros((4, 128), dtype=torch.uint8, device=DEV),
+                         kernel=KERNEL_SPLIT)
