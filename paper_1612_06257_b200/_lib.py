@@ -61,11 +61,14 @@ def lib(build_if_missing: bool = True):
     """Load (building first if the .so is missing) the engine library."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_build.SO):
-            if not build_if_missing:
-                raise EngineError(f"engine library not built: {_build.SO}")
-            _build.build()
-        l = ctypes.CDLL(_build.SO)
+        path = os.environ.get("LH_LIBRARY")  # A/B tuning runs load an alternate build
+        if not path:
+            path = _build.SO
+            if not os.path.exists(path):
+                if not build_if_missing:
+                    raise EngineError(f"engine library not built: {path}")
+                _build.build()
+        l = ctypes.CDLL(path)
         _declare(l)
         _lib = l
     return _lib

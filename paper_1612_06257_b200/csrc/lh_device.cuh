@@ -278,16 +278,42 @@ __device__ __forceinline__ u64 rotl64(u64 x, int b) {
   return (x << b) | (x >> (64 - b));
 }
 
-__device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3) {
-  v0 += v1;
-  v1 = rotl64(v1, 13) ^ v0;
+__device__ __forceinline__ u64 mulwide(u32 a, u32 b) {
+  u64 r;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// Runtime constants that keep half of SipRound on the FMA pipe: `one` for
+// add64_mixed, and 2^13 / 2^17 (2^21 unused) so two of the four rotates become
+// IMAD.WIDE.U32 products (x * 2^k = x << k in the low word, x >> (32-k) in
+// the high word) merged by a 3-input LOP3 with the following XOR.  Set by
+// the host; opaque to ptxas, which would otherwise strength-reduce them.
+struct SipMul {
+  u32 one, m13, m17, m21;
+};
+
+// rotl64(x, k) ^ v with the shifts done as two 32x32->64 multiplies by 2^k.
+__device__ __forceinline__ u64 rotl_xor_wide(u64 x, u32 pow2k, u64 v) {
+  const u64 a = mulwide(lo32(x), pow2k), b = mulwide(hi32(x), pow2k);
+  const u32 lo = (lo32(a) | hi32(b)) ^ lo32(v);
+  const u32 hi = (lo32(b) | hi32(a)) ^ hi32(v);
+  return pack(lo, hi);
+}
+
+// S/sip.py:73-86.  ALU pipe: 4 IADD3 + 2 PRMT (rotate 16) + ~3 SHF (rotate
+// 21) + 8 LOP3; FMA pipe: 4 IMAD.X + 4 IMAD.WIDE (rotates 13, 17).  Moving
+// the rotate by 21 to IMAD.WIDE too measured slower (profiles/README.md).
+__device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k) {
+  v0 = add64_mixed(v0, v1, k.one);
+  v1 = rotl_xor_wide(v1, k.m13, v0);
   v0 = rot32(v0);
-  v2 += v3;
+  v2 = add64_mixed(v2, v3, k.one);
   v3 = rotl64(v3, 16) ^ v2;
-  v0 += v3;
+  v0 = add64_mixed(v0, v3, k.one);
   v3 = rotl64(v3, 21) ^ v0;
-  v2 += v1;
-  v1 = rotl64(v1, 17) ^ v2;
+  v2 = add64_mixed(v2, v1, k.one);
+  v1 = rotl_xor_wide(v1, k.m17, v2);
   v2 = rot32(v2);
 }
 
@@ -305,24 +331,24 @@ struct SipCore {
     v2 = 0x6C7967656E657261ull ^ k.k0;
     v3 = 0x7465646279746573ull ^ k.k1;
   }
-  __device__ __forceinline__ void compress(u64 m, int c) {
+  __device__ __forceinline__ void compress(u64 m, int c, const SipMul& k) {
     v3 ^= m;
     if (C > 0) {
 #pragma unroll
-      for (int i = 0; i < C; ++i) sip_round(v0, v1, v2, v3);
+      for (int i = 0; i < C; ++i) sip_round(v0, v1, v2, v3, k);
     } else {
-      for (int i = 0; i < c; ++i) sip_round(v0, v1, v2, v3);
+      for (int i = 0; i < c; ++i) sip_round(v0, v1, v2, v3, k);
     }
     v0 ^= m;
   }
-  __device__ __forceinline__ u64 final(u64 m_last, int c, int d) {
-    compress(m_last, c);
+  __device__ __forceinline__ u64 final(u64 m_last, int c, int d, const SipMul& k) {
+    compress(m_last, c, k);
     v2 ^= 0xFF;
     if (D > 0) {
 #pragma unroll
-      for (int i = 0; i < D; ++i) sip_round(v0, v1, v2, v3);
+      for (int i = 0; i < D; ++i) sip_round(v0, v1, v2, v3, k);
     } else {
-      for (int i = 0; i < d; ++i) sip_round(v0, v1, v2, v3);
+      for (int i = 0; i < d; ++i) sip_round(v0, v1, v2, v3, k);
     }
     return v0 ^ v1 ^ v2 ^ v3;
   }
@@ -332,6 +358,7 @@ template <int C, int D>
 struct Sip {
   SipCore<C, D> s;
   int c, d;
+  SipMul k;
   __device__ __forceinline__ void init(const SipKey& k, int c_, int d_) {
     s.init(k);
     c = c_;
@@ -339,19 +366,19 @@ struct Sip {
   }
   __device__ __forceinline__ void absorb32(const u64 (&p)[4]) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s.compress(p[k], c);
+    for (int w = 0; w < 4; ++w) s.compress(p[w], c, k);
   }
   // Tail: r = len % 32 bytes in t (zero beyond r).  Whole words first, then
   // the final word = leftover bytes | (len & 0xFF) << 56 (S/sip.py:100-101).
   __device__ __forceinline__ void finish(const u64 (&t)[4], u32 r, u64 len, u64* out) {
     const u32 nw = r >> 3;
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      if ((u32)k < nw) s.compress(t[k], c);
+    for (int w = 0; w < 3; ++w)
+      if ((u32)w < nw) s.compress(t[w], c, k);
     const u64 s01 = (nw & 1) ? t[1] : t[0];
     const u64 s23 = (nw & 1) ? t[3] : t[2];
     const u64 last = (nw & 2) ? s23 : s01;
-    out[0] = s.final(last | ((len & 0xFF) << 56), c, d);
+    out[0] = s.final(last | ((len & 0xFF) << 56), c, d, k);
   }
 };
 
@@ -364,6 +391,7 @@ struct SipTree {
   SipCore<C, D> l0, l1, l2, l3;
   SipKey key;
   int c, d;
+  SipMul k;
   __device__ __forceinline__ void init(const SipKey& k, int c_, int d_) {
     key = k;
     l0.init(k);
@@ -374,26 +402,26 @@ struct SipTree {
     d = d_;
   }
   __device__ __forceinline__ void absorb32(const u64 (&p)[4]) {
-    l0.compress(p[0], c);
-    l1.compress(p[1], c);
-    l2.compress(p[2], c);
-    l3.compress(p[3], c);
+    l0.compress(p[0], c, k);
+    l1.compress(p[1], c, k);
+    l2.compress(p[2], c, k);
+    l3.compress(p[3], c, k);
   }
   __device__ __forceinline__ void finish(const u64 (&t)[4], u32 r, u64 len, u64* out) {
     if (r) absorb32(t);  // zero-padded final block
     const u64 lane_len = ((len + 31) & ~31ull) >> 2;
     const u64 m = (lane_len & 0xFF) << 56;
-    const u64 h0 = l0.final(m, c, d);
-    const u64 h1 = l1.final(m, c, d);
-    const u64 h2 = l2.final(m, c, d);
-    const u64 h3 = l3.final(m, c, d);
+    const u64 h0 = l0.final(m, c, d, k);
+    const u64 h1 = l1.final(m, c, d, k);
+    const u64 h2 = l2.final(m, c, d, k);
+    const u64 h3 = l3.final(m, c, d, k);
     SipCore<C, D> f;
     f.init(key);
-    f.compress(h0, c);
-    f.compress(h1, c);
-    f.compress(h2, c);
-    f.compress(h3, c);
-    out[0] = f.final(32ull << 56, c, d);
+    f.compress(h0, c, k);
+    f.compress(h1, c, k);
+    f.compress(h2, c, k);
+    f.compress(h3, c, k);
+    out[0] = f.final(32ull << 56, c, d, k);
   }
 };
 

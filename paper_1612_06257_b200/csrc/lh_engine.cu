@@ -72,6 +72,7 @@ Sip<C, D> make_sip(const u64 key[2], int c, int d) {
   h_sip_init(h.s, SipKey{key[0], key[1]});
   h.c = c;
   h.d = d;
+  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 21};
   return h;
 }
 
@@ -87,6 +88,7 @@ SipTree<C, D> make_siptree(const u64 key[2], int c, int d) {
   h_sip_init(h.l3, k);
   h.c = c;
   h.d = d;
+  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 21};
   return h;
 }
 
