@@ -206,6 +206,131 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
 }
 
 // --------------------------------------------------------------------------
+// Ragged short-message kernel (cfg3: 2^26 keys of 8..64 bytes, finalization
+// dominated).  Each warp takes 32 consecutive messages.  Fast path (every
+// message <= 64 B and the warp's byte span <= kSpanCap): the warp copies the
+// span into shared memory with coalesced 16-byte loads, each thread builds
+// its message's 16 little-endian 32-bit words with funnel shifts (bytes past
+// the end zeroed), and runs exactly two non-divergent Update slots:
+//   slot s (s = 0, 1): full block s if s < nfull, else the remainder
+//   packet of the tail if s == nfull and r > 0, else nothing;
+// the remainder's length injection is applied unconditionally with r_eff =
+// r or 0 (adding 0 / rotating by 0 is the identity), so lanes with different
+// lengths never split the Update.  Any other warp (long messages, scattered
+// offsets) takes the generic per-thread path (hash_direct).
+// --------------------------------------------------------------------------
+constexpr u32 kSpanCap = 2048;  // bytes of a warp's span staged in smem
+
+// Remainder packet (S/highway.py:206-220) from the tail's 8 words (zero past
+// r): word q = r/4 (the 0..3 leftover bytes, LE) moves to packet word 7.
+__device__ __forceinline__ void rem_packet_words(const u32 (&T)[8], u32 r, u64 (&p)[4]) {
+  const u32 q = r >> 2;
+  u32 P[8];
+  u32 lft = T[0];
+#pragma unroll
+  for (u32 j = 1; j < 8; ++j) lft = (q == j) ? T[j] : lft;
+#pragma unroll
+  for (u32 j = 0; j < 7; ++j) P[j] = (q == j) ? 0u : T[j];
+  P[7] = lft;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p[k] = pack(P[2 * k], P[2 * k + 1]);
+}
+
+// Length injection of UpdateRemainder (S/highway.py:188-197); r = 0 is a no-op.
+__device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h.v0[i] = pack(lo32(h.v0[i]) + r, hi32(h.v0[i]) + r);
+    h.v1[i] = pack(__funnelshift_l(lo32(h.v1[i]), lo32(h.v1[i]), r),
+                   __funnelshift_l(hi32(h.v1[i]), hi32(h.v1[i]), r));
+  }
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto,
+                                                             const uint8_t* __restrict__ buf,
+                                                             const u64* __restrict__ offsets,
+                                                             const u32* __restrict__ lengths,
+                                                             u64 n, u64* __restrict__ out) {
+  __shared__ __align__(16) uint4 stage[WARPS][kSpanCap / 16 + 8];
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = proto.width / 64;
+  const u32* S = reinterpret_cast<const u32*>(&stage[warp][0]);
+  for (u64 base = ((u64)blockIdx.x * WARPS + warp) * 32; base < n;
+       base += (u64)gridDim.x * WARPS * 32) {
+    const u64 i = base + lane;
+    const bool valid = i < n;
+    u64 start = 0, len = 0;
+    if (valid) {
+      start = offsets[i];
+      len = lengths ? (u64)lengths[i] : offsets[i + 1] - start;
+    }
+    u64 lo = valid ? start : ~0ull, hi = valid ? start + len : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const u64 a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+    const u32 maxlen = __reduce_max_sync(0xffffffffu, (u32)(len > 0xffffffffull ? 0xffffffffu : len));
+    if (maxlen <= 64 && hi - lo <= kSpanCap) {
+      const u64 lo_al = lo & ~15ull, hi_al = (hi + 15) & ~15ull;
+      const u32 nch = (u32)((hi_al - lo_al) >> 4);
+      const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
+      for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
+      __syncwarp();
+      if (valid) {
+        const u32 o = (u32)(start - lo_al), a = o >> 2, sh = (o & 3) * 8;
+        const u32 L = (u32)len;
+        u32 Wd[16];
+        u32 cur = S[a];
+#pragma unroll
+        for (u32 k = 0; k < 16; ++k) {
+          const u32 nxt = S[a + k + 1];
+          u32 w = __funnelshift_r(cur, nxt, sh);
+          const int keep = (int)L - 4 * (int)k;  // bytes of word k inside the message
+          w &= keep >= 4 ? 0xffffffffu : (keep <= 0 ? 0u : ((1u << (8 * keep)) - 1u));
+          Wd[k] = w;
+          cur = nxt;
+        }
+        const u32 nfull = L >> 5, r = L & 31;
+        Highway h = proto;
+#pragma unroll
+        for (u32 s = 0; s < 2; ++s) {
+          const bool full = s < nfull;
+          const bool rem = (s == nfull) && r;
+          if (full || rem) {
+            u32 T[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) T[j] = Wd[8 * s + j];
+            u64 p[4];
+            rem_packet_words(T, rem ? r : 0u, p);
+            if (full) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) p[k] = pack(T[2 * k], T[2 * k + 1]);
+            }
+            rem_tweak(h, rem ? r : 0u);
+            h.update(p[0], p[1], p[2], p[3]);
+          }
+        }
+        h.finalize_rounds();
+        u64* o64 = out + i * W;
+        o64[0] = h.v0[0] + h.v1[0] + h.m0[0] + h.m1[0];
+        if (W >= 2) o64[1] = h.v0[1] + h.v1[1] + h.m0[1] + h.m1[1];
+        if (W == 4) {
+          o64[2] = h.v0[2] + h.v1[2] + h.m0[2] + h.m1[2];
+          o64[3] = h.v0[3] + h.v1[3] + h.m0[3] + h.m1[3];
+        }
+      }
+      __syncwarp();
+    } else if (valid) {
+      Highway h = proto;
+      hash_direct(h, buf + start, len, out + i * W);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // TMA-staged fixed-length kernel.
 // Requirements (checked on the host): len % 16 == 0, d_msgs 16-B aligned.
 // Shared ring: STAGES x [ROWS rows x 128 B] with the 128-byte swizzle:
@@ -762,7 +887,17 @@ int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uin
   if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
     return LH_EALIGN;
   const Highway h = make_highway(key, width, rounds);
-  return launch_direct(h, d_buf, d_offsets, d_lengths, 0, n, d_out, (cudaStream_t)stream);
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  constexpr int kWarps = 8;
+  const u64 warps = (n + 31) / 32;
+  const u64 cap = (u64)sms * 8 * (64 / kWarps);
+  const u64 blocks = (warps + kWarps - 1) / kWarps;
+  k_ragged_short<kWarps><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0,
+                           (cudaStream_t)stream>>>(h, d_buf, d_offsets, d_lengths, n, d_out);
+  return cuda_err(cudaGetLastError());
 }
 
 static int sip_fixed_impl(const uint8_t* d_msgs, u64 n, u64 len, const u64 key[2], int c, int d,

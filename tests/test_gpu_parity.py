@@ -307,3 +307,40 @@ def test_split_kernel_rejects_unsupported_shapes():
     with pytest.raises(ValueError):
         engine.sip_batch(synth.key128(), torch.zeros((4, 128), dtype=torch.uint8, device=DEV),
                          kernel=KERNEL_SPLIT)
+
+
+# ---------------------------------------------------------------------------
+# ragged short-message kernel: warp-staged fast path and its fallback
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["packed", "scattered", "mixed_long", "wide_span"])
+def test_ragged_short_paths(oracle, case):
+    rng = np.random.default_rng({"packed": 1, "scattered": 2, "mixed_long": 3, "wide_span": 4}[case])
+    n = 20000
+    if case == "packed":          # cfg3 shape: packed, every residue 0..64
+        lens = rng.integers(0, 65, n).astype(np.uint32)
+        off = np.zeros(n, np.uint64)
+        off[1:] = np.cumsum(lens[:-1])
+        buf = synth.counter_bytes(60, int(lens.sum()) + 1)
+    elif case == "scattered":     # unsorted / overlapping offsets inside a 1.5 KB window per warp
+        lens = rng.integers(0, 65, n).astype(np.uint32)
+        warp_base = (np.arange(n) // 32) * 2000
+        off = (warp_base + rng.integers(0, 1500, n)).astype(np.uint64)
+        buf = synth.counter_bytes(61, int(off.max()) + 70)
+    elif case == "mixed_long":    # some warps contain a message > 64 B (fallback)
+        lens = rng.integers(0, 65, n).astype(np.uint32)
+        lens[rng.choice(n, 200, replace=False)] = rng.integers(65, 600, 200)
+        off = np.zeros(n, np.uint64)
+        off[1:] = np.cumsum(lens[:-1])
+        buf = synth.counter_bytes(62, int(lens.sum()) + 1)
+    else:                         # short messages but spans wider than the staging cap
+        lens = rng.integers(1, 65, n).astype(np.uint32)
+        off = (np.arange(n, dtype=np.uint64) * 97) % np.uint64(n * 64)
+        buf = synth.counter_bytes(63, n * 64 + 70)
+    for width in (64, 256):
+        got = engine.highway_ragged(synth.key256(), buf, off, lens, width)
+        want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, lens, width, 4)
+        assert np.array_equal(got, want), (case, width)
+    got = engine.highway_ragged(synth.key256(), buf, off, lens, 64, rounds=2)
+    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, lens, 64, 2)
+    assert np.array_equal(got, want)
