@@ -97,6 +97,31 @@ int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets,
 int lh_highway_prf64(uint64_t start, uint64_t n, const uint64_t key[4],
                      int rounds, uint64_t* d_out, void* stream);
 
+/* ---- Batched streaming (incremental) hashing ----
+ * Replaces: highway.StreamingHasher (S/highway.py:257-285), sip.SipHasher
+ * (S/sip.py:131-169) and sip.SipTreeHasher (S/sip.py:172-203), for n
+ * messages at once.  d_state holds n records of lh_stream_state_bytes(alg)
+ * bytes (16-B aligned, caller-allocated): hasher state, <= 31 pending bytes,
+ * total length.  For any split of each message into chunks, init + updates +
+ * finish equals the one-shot digest (T/test_highway.py:156-193). */
+#define LH_ALG_HIGHWAY 0
+#define LH_ALG_SIPHASH 1
+#define LH_ALG_SIPTREE 2
+size_t lh_stream_state_bytes(int alg);
+/* p1, p2 = width, rounds (HighwayHash) or c, d (SipHash / SipTreeHash). */
+int lh_stream_init(int alg, void* d_state, uint64_t n, const uint64_t* key,
+                   int p1, int p2, void* stream);
+/* Append one chunk per message: fixed layout (d_offsets == NULL) chunk i is
+ * d_buf[i*chunk_len : (i+1)*chunk_len]; ragged layout as lh_highway_ragged. */
+int lh_stream_update(int alg, void* d_state, uint64_t n, const uint8_t* d_buf,
+                     const uint64_t* d_offsets, const uint32_t* d_lengths,
+                     uint64_t chunk_len, void* stream);
+/* Digests of the appended data (state is not consumed).  lanes = 1, 2 or 4
+ * (digest width / 64) for HighwayHash -- the absorbed state is
+ * width-independent, as in S/highway.py:278-285 -- and 1 for the Sip family. */
+int lh_stream_finish(int alg, const void* d_state, uint64_t n, uint64_t* d_out,
+                     int lanes, void* stream);
+
 /* Seeded synthetic input generator (bench/test harness; not a reference
  * interface).  Byte b of the stream is byte (b & 7) of
  * word(seed, stream_id, word_offset + b / 8), see DESIGN.md §Synthetic

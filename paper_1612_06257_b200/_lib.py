@@ -27,6 +27,10 @@ KERNEL_DIRECT = 1
 KERNEL_TMA = 2
 KERNEL_SPLIT = 3
 
+ALG_HIGHWAY = 0
+ALG_SIPHASH = 1
+ALG_SIPTREE = 2
+
 _lib = None
 
 
@@ -47,12 +51,18 @@ def _declare(l):
     l.lh_siphash_fixed_kernel.argtypes = [vp, u64, u64, vp, i32, i32, i32, vp, vp, i32]
     l.lh_siphash_ragged.argtypes = [vp, vp, vp, u64, vp, i32, i32, i32, vp, vp]
     l.lh_highway_prf64.argtypes = [u64, u64, vp, i32, vp, vp]
+    l.lh_stream_state_bytes.argtypes = [i32]
+    l.lh_stream_state_bytes.restype = ctypes.c_size_t
+    l.lh_stream_init.argtypes = [i32, vp, u64, vp, i32, i32, vp]
+    l.lh_stream_update.argtypes = [i32, vp, u64, vp, vp, vp, u64, vp]
+    l.lh_stream_finish.argtypes = [i32, vp, u64, vp, i32, vp]
     l.lh_synth_fill.argtypes = [vp, u64, u64, u64, u64, vp]
     l.lh_synth_lengths.argtypes = [vp, u64, u64, u64, u32, u32, vp]
     for name in (
         "lh_highway_fixed", "lh_highway_fixed_kernel", "lh_highway_ragged",
         "lh_siphash_fixed", "lh_siphash_fixed_kernel", "lh_siphash_ragged",
         "lh_highway_prf64", "lh_synth_fill", "lh_synth_lengths",
+        "lh_stream_init", "lh_stream_update", "lh_stream_finish",
     ):
         getattr(l, name).restype = i32
 

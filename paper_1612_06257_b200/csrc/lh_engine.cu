@@ -21,6 +21,8 @@
 
 #include "../../include/lanehash_b200.h"
 #include "lh_device.cuh"
+#include "lh_reader.cuh"
+#include "lh_host.cuh"
 #include "lh_tma.cuh"
 
 using namespace lh;
@@ -29,69 +31,6 @@ using namespace lh;
 
 namespace {
 
-// --------------------------------------------------------------------------
-// Host-side hasher prototypes (the kernels copy them by value).
-// --------------------------------------------------------------------------
-
-// S/highway.py:20-31
-const u64 kInit0[4] = {0xDBE6D5D5FE4CCE2FULL, 0xA4093822299F31D0ULL, 0x13198A2E03707344ULL,
-                       0x243F6A8885A308D3ULL};
-const u64 kInit1[4] = {0x3BD39E10CB0EF593ULL, 0xC0ACF169B5F18A8CULL, 0xBE5466CF34E90C6CULL,
-                       0x452821E638D01377ULL};
-
-inline u64 h_rot32(u64 x) { return (x >> 32) | (x << 32); }
-
-// Key expansion, S/highway.py:122-127 (one key per batch: done once here).
-Highway make_highway(const u64 key[4], int width, int rounds) {
-  Highway h;
-  memset(&h, 0, sizeof h);
-  for (int i = 0; i < 4; ++i) {
-    h.v0[i] = key[i] ^ kInit0[i];
-    h.v1[i] = h_rot32(key[i]) ^ kInit1[i];
-    h.m0[i] = kInit0[i];
-    h.m1[i] = kInit1[i];
-  }
-  h.rounds = rounds;
-  h.width = width;
-  h.one = 1;
-  return h;
-}
-
-template <int C, int D>
-void h_sip_init(SipCore<C, D>& s, const SipKey& k) {
-  s.v0 = 0x736F6D6570736575ull ^ k.k0;
-  s.v1 = 0x646F72616E646F6Dull ^ k.k1;
-  s.v2 = 0x6C7967656E657261ull ^ k.k0;
-  s.v3 = 0x7465646279746573ull ^ k.k1;
-}
-
-template <int C, int D>
-Sip<C, D> make_sip(const u64 key[2], int c, int d) {
-  Sip<C, D> h;
-  memset(&h, 0, sizeof h);
-  h_sip_init(h.s, SipKey{key[0], key[1]});
-  h.c = c;
-  h.d = d;
-  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 21};
-  return h;
-}
-
-template <int C, int D>
-SipTree<C, D> make_siptree(const u64 key[2], int c, int d) {
-  SipTree<C, D> h;
-  memset(&h, 0, sizeof h);
-  const SipKey k{key[0], key[1]};
-  h.key = k;
-  h_sip_init(h.l0, k);
-  h_sip_init(h.l1, k);
-  h_sip_init(h.l2, k);
-  h_sip_init(h.l3, k);
-  h.c = c;
-  h.d = d;
-  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 21};
-  return h;
-}
-
 template <class H>
 __host__ __device__ inline int nout(const H&) {
   return 1;
@@ -99,28 +38,6 @@ __host__ __device__ inline int nout(const H&) {
 template <>
 __host__ __device__ inline int nout<Highway>(const Highway& h) {
   return h.width / 64;
-}
-
-// --------------------------------------------------------------------------
-// Direct (global-load) reader: any alignment, any length, fixed or ragged.
-// Only 8-byte-aligned words that contain at least one message byte are
-// read, so no access leaves the message's own aligned words.
-// --------------------------------------------------------------------------
-
-__device__ __forceinline__ u64 ldg64(const u64* p) { return __ldg((const unsigned long long*)p); }
-
-__device__ __forceinline__ u64 funnel(u64 a, u64 b, u32 sh) {
-  // bytes of the 16-byte window a|b starting at byte sh/8 (sh in 8..56)
-  return (a >> sh) | (b << (64 - sh));
-}
-
-__device__ __forceinline__ void mask_tail(u64 (&t)[4], u32 r) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int keep = (int)r - 8 * k;
-    const u64 m = keep >= 8 ? ~0ull : (keep <= 0 ? 0ull : ((1ull << (8 * keep)) - 1));
-    t[k] &= m;
-  }
 }
 
 template <class H>

@@ -274,3 +274,97 @@ def sip_one(key: Key128, message, c: int, d: int, tree: bool) -> int:
     out = torch.empty((1,), dtype=torch.int64, device=device)
     _launch_fixed("sip", key, m, 1, m.shape[1], c, d, int(bool(tree)), out, KERNEL_AUTO, device)
     return int(to_u64(out)[0])
+
+
+# ---------------------------------------------------------------------------
+# Batched streaming (incremental) hashing — csrc/lh_stream.cu
+# ---------------------------------------------------------------------------
+
+ALG_HIGHWAY = _lib.ALG_HIGHWAY
+ALG_SIPHASH = _lib.ALG_SIPHASH
+ALG_SIPTREE = _lib.ALG_SIPTREE
+
+
+class StreamBatch:
+    """n messages hashed incrementally on the device.
+
+    The batch form of StreamingHasher / SipHasher / SipTreeHasher
+    (S/highway.py:257-285, S/sip.py:131-203): ``append`` one chunk per
+    message (an (n, Lc) uint8 tensor, or a ragged ``(buf, offsets[, lengths])``
+    triple), any number of times; ``finish`` returns the digests of
+    everything appended.  Appending after ``finish`` or finishing twice raises
+    RuntimeError, as the reference's hashers do (S/highway.py:269-281)."""
+
+    def __init__(self, alg: int, key, n: int, width: int = 64, rounds: int = 4,
+                 c: int = 2, d: int = 4):
+        self.device = _require_cuda()
+        if n < 0:
+            raise ValueError("n must be >= 0")
+        self.alg, self.n = alg, n
+        if alg == ALG_HIGHWAY:
+            _check_width(width)
+            k, p1, p2, self.lanes = _key4(as_key256(key)), width, rounds, width // 64
+        elif alg in (ALG_SIPHASH, ALG_SIPTREE):
+            if c < 1 or d < 1:
+                raise ValueError("round counts must be positive")
+            k, p1, p2, self.lanes = _key2(as_key128(key)), c, d, 1
+        else:
+            raise ValueError(f"unknown algorithm id {alg}")
+        rec = _lib.lib().lh_stream_state_bytes(alg)
+        self.state = torch.empty(max(1, n) * rec, dtype=torch.uint8, device=self.device)
+        self._finished = False
+        _lib.check(_lib.lib().lh_stream_init(alg, self.state.data_ptr(), n, k, p1, p2,
+                                             _stream_ptr(self.device)), "lh_stream_init")
+
+    def append(self, chunks, offsets=None, lengths=None) -> "StreamBatch":
+        if self._finished:
+            raise RuntimeError("cannot append after finish")
+        st = _stream_ptr(self.device)
+        if offsets is None:
+            m = _as_u8_2d(chunks)
+            if m.shape[0] != self.n:
+                raise ValueError("one chunk per message expected")
+            m = m.to(self.device).contiguous()
+            ptr = m.data_ptr() if m.numel() else 0
+            rc = _lib.lib().lh_stream_update(self.alg, self.state.data_ptr(), self.n, ptr, None,
+                                             None, m.shape[1], st)
+            keep = (m,)
+        else:
+            d_buf = _to_device(chunks.reshape(-1) if isinstance(chunks, np.ndarray) else chunks,
+                               torch.uint8, self.device)
+            if isinstance(offsets, np.ndarray):
+                offsets = offsets.astype(np.uint64, copy=False).view(np.int64)
+            if isinstance(lengths, np.ndarray):
+                lengths = lengths.astype(np.uint32, copy=False).view(np.int32)
+            d_off = _to_device(offsets, torch.int64, self.device)
+            d_len = None if lengths is None else _to_device(lengths, torch.int32, self.device)
+            nn = d_off.numel() - 1 if d_len is None else d_off.numel()
+            if nn != self.n:
+                raise ValueError("one chunk per message expected")
+            bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
+            rc = _lib.lib().lh_stream_update(self.alg, self.state.data_ptr(), self.n, bp,
+                                             d_off.data_ptr(),
+                                             d_len.data_ptr() if d_len is not None else None,
+                                             0, st)
+            keep = (d_buf, d_off, d_len)
+        _lib.check(rc, "lh_stream_update")
+        self._keep = keep  # inputs stay alive until the next call on this stream
+        return self
+
+    def finish(self, width: Optional[int] = None):
+        """Digests (device tensor).  HighwayHash may pick the width here (the
+        absorbed state is width-independent); default: the init width."""
+        if self._finished:
+            raise RuntimeError("finish may only be called once")
+        lanes = self.lanes
+        if width is not None:
+            if self.alg != ALG_HIGHWAY:
+                raise ValueError("width applies to HighwayHash only")
+            _check_width(width)
+            lanes = width // 64
+        self._finished = True
+        out = torch.empty(_out_shape(self.n, lanes), dtype=torch.int64, device=self.device)
+        _lib.check(_lib.lib().lh_stream_finish(self.alg, self.state.data_ptr(), self.n,
+                                               out.data_ptr(), lanes,
+                                               _stream_ptr(self.device)), "lh_stream_finish")
+        return out

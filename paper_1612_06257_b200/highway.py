@@ -108,6 +108,37 @@ def hash256(key, message: bytes, rounds: int = 4) -> Tuple[int, int, int, int]:
     return tuple(int(x) for x in out)
 
 
+class StreamingHasher:
+    """Incremental HighwayHash (S/highway.py:257-285) on the GPU engine.
+
+    Same contract as the reference: only len mod 32 affects padding; append
+    after finish and a second finish raise RuntimeError.  Each append ships
+    the chunk to the device and advances the state there (engine.StreamBatch
+    with n = 1): nothing but the device record (state, <= 31 pending bytes,
+    length) is retained.  Use engine.StreamBatch to stream many messages."""
+
+    def __init__(self, key, rounds: int = 4):
+        from . import engine
+
+        self._engine = engine
+        self._sb = engine.StreamBatch(engine.ALG_HIGHWAY, as_key256(key), 1, 256, rounds)
+
+    def append(self, chunk: bytes) -> "StreamingHasher":
+        import numpy as np
+
+        if self._sb._finished:
+            raise RuntimeError("cannot append after finish")
+        raw = bytes(chunk)
+        if raw:
+            self._sb.append(np.frombuffer(raw, np.uint8).reshape(1, -1))
+        return self
+
+    def finish(self, width: int = 64):
+        _check_width(width)
+        out = [int(x) for x in self._engine.to_u64(self._sb.finish(width)).reshape(-1)]
+        return out[0] if width == 64 else tuple(out)
+
+
 def digest64_to_bytes(digest: int) -> bytes:
     """Little-endian byte image of a 64-bit digest (S/highway.py:288-290)."""
     return struct.pack("<Q", digest & _MASK64)

@@ -88,3 +88,42 @@ def siptreehash(key, message: bytes, params: SipParams = SIPHASH_24) -> int:
     from . import engine
 
     return engine.sip_one(as_key128(key), message, params.c, params.d, tree=True)
+
+
+class _SipStream:
+    def __init__(self, alg, key, params: SipParams):
+        from . import engine
+
+        self._engine = engine
+        self._sb = engine.StreamBatch(alg, as_key128(key), 1, c=params.c, d=params.d)
+
+    def append(self, chunk: bytes):
+        import numpy as np
+
+        if self._sb._finished:
+            raise RuntimeError("cannot append after finish")
+        raw = bytes(chunk)
+        if raw:
+            self._sb.append(np.frombuffer(raw, np.uint8).reshape(1, -1))
+        return self
+
+    def finish(self) -> int:
+        return int(self._engine.to_u64(self._sb.finish()).reshape(-1)[0])
+
+
+class SipHasher(_SipStream):
+    """Incremental SipHash-c-d (S/sip.py:131-169) on the GPU engine."""
+
+    def __init__(self, key, params: SipParams = SIPHASH_24):
+        from . import engine
+
+        super().__init__(engine.ALG_SIPHASH, key, params)
+
+
+class SipTreeHasher(_SipStream):
+    """Incremental 4-lane tree hash (S/sip.py:172-203) on the GPU engine."""
+
+    def __init__(self, key, params: SipParams = SIPHASH_24):
+        from . import engine
+
+        super().__init__(engine.ALG_SIPTREE, key, params)

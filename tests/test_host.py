@@ -151,3 +151,17 @@ def test_remainder_sweep_layout():
     lens, off, kind = synth.remainder_sweep_layout(1024, 64)
     assert len(lens) == 65536 and int(off[-1]) == 33521664
     assert (kind == 0).sum() == 32768 and (kind == 1).sum() == 16384
+
+
+def test_stream_abi_validation_without_device():
+    l = _lib.lib()
+    assert [l.lh_stream_state_bytes(a) > 0 for a in range(3)] == [True] * 3
+    assert l.lh_stream_state_bytes(7) == 0
+    key4 = (ctypes.c_uint64 * 4)(1, 2, 3, 4)
+    buf = ctypes.create_string_buffer(512)
+    base = (ctypes.addressof(buf) + 15) & ~15
+    assert l.lh_stream_init(0, base, 1, key4, 96, 4, None) == _lib.LH_EINVAL
+    assert l.lh_stream_init(1, base, 1, key4, 0, 4, None) == _lib.LH_EINVAL
+    assert l.lh_stream_init(0, base + 8, 1, key4, 64, 4, None) == _lib.LH_EALIGN
+    assert l.lh_stream_init(9, base, 1, key4, 64, 4, None) == _lib.LH_EINVAL
+    assert l.lh_stream_finish(1, base, 1, base, 2, None) == _lib.LH_EINVAL
