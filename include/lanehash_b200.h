@@ -122,6 +122,19 @@ int lh_stream_update(int alg, void* d_state, uint64_t n, const uint8_t* d_buf,
 int lh_stream_finish(int alg, const void* d_state, uint64_t n, uint64_t* d_out,
                      int lanes, void* stream);
 
+/* ---- Quality harness: avalanche flip tallies ----
+ * Replaces: _kernels.avalanche_counts (S/_kernels.py:247-265), the kernel of
+ * the avalanche protocol (S/quality.py:105-194) and of the finalization-round
+ * experiment (S/quality.py:245-293).  For each of `iters` messages of `size`
+ * bytes (1..32) and each input bit b: d_counts[b*64 + ob] += bit ob of
+ * hash(msg ^ bit b) ^ hash(msg).  Tallies are ACCUMULATED (caller zeroes).
+ * alg: LH_ALG_HIGHWAY (64-bit digest, p1 = finalization rounds),
+ * LH_ALG_SIPHASH / LH_ALG_SIPTREE (p1 = c, p2 = d).  d_msgs == NULL: message
+ * i is the little-endian bytes of i (exhaustive enumeration). */
+int lh_avalanche_counts(int alg, const uint64_t* key, const uint8_t* d_msgs,
+                        uint64_t iters, uint32_t size, int p1, int p2,
+                        int64_t* d_counts, void* stream);
+
 /* Seeded synthetic input generator (bench/test harness; not a reference
  * interface).  Byte b of the stream is byte (b & 7) of
  * word(seed, stream_id, word_offset + b / 8), see DESIGN.md §Synthetic

@@ -48,6 +48,7 @@ def lib():
         l.lh_ref_hh_update.argtypes = [vp, vp]
         l.lh_ref_hh_init.argtypes = [vp, vp]
         l.lh_ref_hh_remainder_packet.argtypes = [vp, ctypes.c_uint, vp]
+        l.lh_ref_avalanche_counts.argtypes = [i32, vp, vp, u64, ctypes.c_uint32, i32, i32, vp, i32]
         _lib = l
     return _lib
 
@@ -125,3 +126,17 @@ def prf64(key, start: int, n: int, rounds: int = 4, nthreads=None) -> np.ndarray
     k = _key(key, 4)
     lib().lh_ref_prf64(_ptr(k), start, n, rounds, _ptr(out), _threads(nthreads))
     return out[:n]
+
+
+def avalanche_counts(alg, key, msgs: np.ndarray, p1: int, p2: int, nthreads=None) -> np.ndarray:
+    """S/_kernels.py:247-265 restated: (8*size, 64) int64 flip tallies."""
+    msgs = np.ascontiguousarray(msgs, dtype=np.uint8)
+    iters, size = msgs.shape
+    k = _key(key, 4 if alg == ALG_HIGHWAY else 2)
+    out = np.zeros((8 * size, 64), np.int64)
+    buf = msgs if msgs.size else np.zeros(1, np.uint8)
+    rc = lib().lh_ref_avalanche_counts(alg, _ptr(k), _ptr(buf), iters, size, p1, p2, _ptr(out),
+                                       _threads(nthreads))
+    if rc:
+        raise ValueError("size too large")
+    return out

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libb200hash.so")
-SOURCES = ["lh_engine.cu", "lh_synth.cu", "lh_stream.cu"]
+SOURCES = ["lh_engine.cu", "lh_synth.cu", "lh_stream.cu", "lh_quality.cu"]
 HEADERS = ["lh_device.cuh", "lh_tma.cuh", "lh_reader.cuh", "lh_host.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -56,13 +56,14 @@ def _declare(l):
     l.lh_stream_init.argtypes = [i32, vp, u64, vp, i32, i32, vp]
     l.lh_stream_update.argtypes = [i32, vp, u64, vp, vp, vp, u64, vp]
     l.lh_stream_finish.argtypes = [i32, vp, u64, vp, i32, vp]
+    l.lh_avalanche_counts.argtypes = [i32, vp, vp, u64, ctypes.c_uint32, i32, i32, vp, vp]
     l.lh_synth_fill.argtypes = [vp, u64, u64, u64, u64, vp]
     l.lh_synth_lengths.argtypes = [vp, u64, u64, u64, u32, u32, vp]
     for name in (
         "lh_highway_fixed", "lh_highway_fixed_kernel", "lh_highway_ragged",
         "lh_siphash_fixed", "lh_siphash_fixed_kernel", "lh_siphash_ragged",
         "lh_highway_prf64", "lh_synth_fill", "lh_synth_lengths",
-        "lh_stream_init", "lh_stream_update", "lh_stream_finish",
+        "lh_stream_init", "lh_stream_update", "lh_stream_finish", "lh_avalanche_counts",
     ):
         getattr(l, name).restype = i32
 

@@ -73,7 +73,10 @@ def _as_u8_2d(msgs):
     a = np.asarray(msgs)
     if a.dtype != np.uint8 or a.ndim != 2:
         raise ValueError("messages must be a 2-D uint8 array (n, length)")
-    return torch.from_numpy(np.ascontiguousarray(a))
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:  # e.g. np.frombuffer(bytes): torch wants writable memory
+        a = a.copy()
+    return torch.from_numpy(a)
 
 
 def _out_shape(n: int, lanes: int):
