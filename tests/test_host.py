@@ -165,3 +165,18 @@ def test_stream_abi_validation_without_device():
     assert l.lh_stream_init(0, base + 8, 1, key4, 64, 4, None) == _lib.LH_EALIGN
     assert l.lh_stream_init(9, base, 1, key4, 64, 4, None) == _lib.LH_EINVAL
     assert l.lh_stream_finish(1, base, 1, base, 2, None) == _lib.LH_EINVAL
+
+
+def test_cli_rejects_bad_arguments_before_hashing():
+    from paper_1612_06257_b200 import cli, vectors
+
+    for argv in (["hash", "--algo", "md5"], ["hash", "--key", "zz"],
+                 ["hash", "--key", "00"], ["avalanche", "--sizes", "2"],
+                 ["avalanche", "--samples", "4"], ["bench", "--preset", "nope"],
+                 ["bench", "--sizes", "x"]):
+        with pytest.raises(SystemExit) as e:
+            cli.main(argv)
+        assert e.value.code == 2, argv
+    with pytest.raises(ValueError):
+        vectors.VectorRecord.from_line("a,b,c")
+    assert vectors.ramp(3) == b"\x00\x01\x02"
