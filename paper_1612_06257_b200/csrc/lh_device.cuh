@@ -42,7 +42,8 @@ __device__ __forceinline__ u64 mul_lo_hi(u64 a, u64 b) {
 // runtime 1 supplied by the host so ptxas cannot fold the IMAD back into an
 // ALU IADD3.X.  HighwayHash is ALU-pipe bound (PRMT, LOP3, IADD3 all issue
 // there); this moves the high halves of all 20 64-bit adds per Update to the FMA
-// pipe (ALU: 20 PRMT + 16 LOP3 + 20 IADD3 = 56; FMA: 8 IMAD.WIDE + 20 IMAD.X).
+// pipe, except the 3-input v1 += p + m0 (one IADD3 + one IADD3.X per lane)
+// (ALU: 20 PRMT + 16 LOP3 + 20 IADD3 = 56; FMA: 8 IMAD.WIDE + 12 IMAD.X).
 __device__ __forceinline__ u64 add64_mixed(u64 a, u64 b, u32 one) {
   u32 lo, hi;
   asm("add.cc.u32 %0, %2, %3;\n\t"
@@ -100,7 +101,7 @@ struct Highway {
     const u64 p[4] = {p0, p1, p2, p3};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      v1[i] = add64_mixed(v1[i], add64_mixed(p[i], m0[i], one), one);
+      v1[i] += p[i] + m0[i];  // 3-input IADD3 + IADD3.X: 2 instructions, no FMA-pipe help needed
       m0[i] ^= mul_lo_hi(v1[i], v0[i]);
       v0[i] = add64_mixed(v0[i], m1[i], one);
       m1[i] ^= mul_lo_hi(v0[i], v1[i]);
@@ -206,7 +207,7 @@ struct HighwayHalf {
     const u64 p[2] = {pa, pb};
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      v1[i] = add64_mixed(v1[i], add64_mixed(p[i], m0[i], one), one);
+      v1[i] += p[i] + m0[i];  // 3-input IADD3 + IADD3.X: 2 instructions, no FMA-pipe help needed
       m0[i] ^= mul_lo_hi(v1[i], v0[i]);
       v0[i] = add64_mixed(v0[i], m1[i], one);
       m1[i] ^= mul_lo_hi(v0[i], v1[i]);

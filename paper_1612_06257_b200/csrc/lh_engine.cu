@@ -256,6 +256,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
 
 constexpr int kBoxBytes = 128;
 
+// Rows per TMA box (boxDim <= 256): ROWS itself, else the largest divisor
+// of ROWS that is a multiple of 32 and <= 256.
+constexpr int tma_box_rows(int rows) {
+  if (rows <= 256) return rows;
+  for (int r = 256; r >= 32; r -= 32)
+    if (rows % r == 0) return r;
+  return 32;
+}
+
 template <int ROWS, int STAGES>
 constexpr size_t tma_smem_bytes() {
   return 1024 /*alignment slack*/ + (size_t)STAGES * ROWS * kBoxBytes + 2 * STAGES * 8;
@@ -269,7 +278,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr u32 kStageBytes = ROWS * kBoxBytes;
   constexpr int kConsumerWarps = ROWS / 32;
-  constexpr int kBoxRowsTma = ROWS < 256 ? ROWS : 256;  // TMA box rows <= 256
+  constexpr int kBoxRowsTma = tma_box_rows(ROWS);  // TMA box rows <= 256
   constexpr int kBoxesPerStage = ROWS / kBoxRowsTma;
   uint64_t* full_bar = (uint64_t*)(smem + STAGES * kStageBytes);
   uint64_t* empty_bar = full_bar + STAGES;
@@ -600,7 +609,7 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)len, (cuuint64_t)nn};
     cuuint64_t strides[1] = {(cuuint64_t)len};
-    cuuint32_t box[2] = {(cuuint32_t)kBoxBytes, (cuuint32_t)(ROWS < 256 ? ROWS : 256)};
+    cuuint32_t box[2] = {(cuuint32_t)kBoxBytes, (cuuint32_t)tma_box_rows(ROWS)};
     cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)(msgs + base * len), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -675,6 +684,9 @@ int tma_cfg_override() {
       if (!strcmp(s, "128x4")) cfg = 1;
       else if (!strcmp(s, "256x3")) cfg = 2;
       else if (!strcmp(s, "512x3")) cfg = 3;
+      else if (!strcmp(s, "384x4")) cfg = 5;
+      else if (!strcmp(s, "320x5")) cfg = 6;
+      else if (!strcmp(s, "448x3")) cfg = 7;
       else if (!strcmp(s, "128x3")) cfg = 4;
     }
   }
@@ -691,6 +703,9 @@ int launch_tma(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out, cu
     case 1: return launch_tma_cfg<H, 128, 4, 3>(proto, msgs, n, len, out, st, sms);
     case 2: return launch_tma_cfg<H, 256, 3, 2>(proto, msgs, n, len, out, st, sms);
     case 3: return launch_tma_cfg<H, 512, 3, 1>(proto, msgs, n, len, out, st, sms);
+    case 5: return launch_tma_cfg<H, 384, 4, 1>(proto, msgs, n, len, out, st, sms);
+    case 6: return launch_tma_cfg<H, 320, 5, 1>(proto, msgs, n, len, out, st, sms);
+    case 7: return launch_tma_cfg<H, 448, 3, 1>(proto, msgs, n, len, out, st, sms);
     case 4: return launch_tma_cfg<H, 128, 3, 4>(proto, msgs, n, len, out, st, sms);
     default: break;
   }
