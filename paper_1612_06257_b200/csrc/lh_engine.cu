@@ -516,12 +516,34 @@ __global__ void __launch_bounds__(32, MINB)
 // key-only, so `proto` arrives already tweaked; per counter: 1 + rounds
 // updates.
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_prf(const Highway proto, u64 start, u64 n,
+// The first Update absorbs the packet (ctr, 0, 0, 0): lanes 1-3 see a
+// constant packet word, so their per-lane steps 1-5 (S/highway.py:137-141)
+// and the whole zipper pair (2,3) are the same for every counter and are
+// precomputed on the host (prf_proto); only lane 0's steps and the pair
+// (0,1) zippers run per counter (~26 of ~78 instructions).
+struct PrfProto {
+  Highway h;      // lanes 1..3 after steps 1-5; lanes 2,3 fully updated;
+                  // lane 0: m0/m1 pre-update, v0 = v0_pre + m1_pre (step 4)
+  u64 v1_0_base;  // v1[0] + m0[0] before the update (steps 1-2 minus ctr)
+  u32 v0_0_hi;    // hi32 of lane-0 v0 before step 4 (used by step 3)
+};
+
+__global__ void __launch_bounds__(256) k_prf(const PrfProto proto, u64 start, u64 n,
                                              u64* __restrict__ out) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (u64)gridDim.x * blockDim.x) {
-    Highway h = proto;
-    h.update(start + i, 0, 0, 0);
+    Highway h = proto.h;
+    const u64 v1_0 = proto.v1_0_base + (start + i);         // steps 1-2
+    h.m0[0] ^= (u64)lo32(v1_0) * (u64)proto.v0_0_hi;        // step 3
+    h.m1[0] ^= mul_lo_hi(h.v0[0], v1_0);                    // step 5 (v0 post step 4)
+    h.v1[0] = v1_0;
+    u64 z0, z1;
+    zipper(h.v1[0], h.v1[1], z0, z1);
+    h.v0[0] = add64_mixed(h.v0[0], z0, h.one);
+    h.v0[1] = add64_mixed(h.v0[1], z1, h.one);
+    zipper(h.v0[0], h.v0[1], z0, z1);
+    h.v1[0] = add64_mixed(h.v1[0], z0, h.one);
+    h.v1[1] = add64_mixed(h.v1[1], z1, h.one);
     h.finalize_rounds();
     out[i] = h.v0[0] + h.v1[0] + h.m0[0] + h.m1[0];
   }
@@ -774,6 +796,55 @@ int sip_dispatch_ragged(const H& h, const uint8_t* buf, const u64* off, const u3
 
 }  // namespace
 
+// Host precompute for k_prf (see PrfProto).  Mirrors S/highway.py:130-150
+// and 182-199 on the host for the counter-independent parts.
+static u64 h_mul32(u64 a, u64 b) { return (u64)(uint32_t)a * (u64)(uint32_t)(b >> 32); }
+static void h_zipper(u64 lo, u64 hi, u64& zlo, u64& zhi) {
+  static const int kZip[16] = {3, 12, 2, 5, 14, 1, 15, 0, 11, 4, 10, 13, 9, 6, 8, 7};
+  uint8_t in[16], o[16];
+  for (int b = 0; b < 8; ++b) {
+    in[b] = (uint8_t)(lo >> (8 * b));
+    in[8 + b] = (uint8_t)(hi >> (8 * b));
+  }
+  for (int b = 0; b < 16; ++b) o[b] = in[kZip[b]];
+  zlo = zhi = 0;
+  for (int b = 7; b >= 0; --b) {
+    zlo = (zlo << 8) | o[b];
+    zhi = (zhi << 8) | o[8 + b];
+  }
+}
+
+static PrfProto prf_proto(const u64 key[4], int rounds) {
+  Highway h = make_highway(key, 64, rounds);
+  for (int i = 0; i < 4; ++i) {  // length injection for r = 8 (S/highway.py:188-197)
+    const uint32_t lo = (uint32_t)h.v0[i] + 8u, hi = (uint32_t)(h.v0[i] >> 32) + 8u;
+    h.v0[i] = ((u64)hi << 32) | lo;
+    const uint32_t l1 = (uint32_t)h.v1[i], h1 = (uint32_t)(h.v1[i] >> 32);
+    const uint32_t rl = (l1 << 8) | (l1 >> 24), rh = (h1 << 8) | (h1 >> 24);
+    h.v1[i] = ((u64)rh << 32) | rl;
+  }
+  PrfProto p;
+  memset(&p, 0, sizeof p);
+  p.v1_0_base = h.v1[0] + h.m0[0];
+  p.v0_0_hi = (uint32_t)(h.v0[0] >> 32);
+  for (int i = 1; i < 4; ++i) {  // steps 1-5 with packet word 0
+    h.v1[i] += h.m0[i];
+    h.m0[i] ^= h_mul32(h.v1[i], h.v0[i]);
+    h.v0[i] += h.m1[i];
+    h.m1[i] ^= h_mul32(h.v0[i], h.v1[i]);
+  }
+  h.v0[0] += h.m1[0];  // lane 0 step 4 is counter-independent
+  u64 z2, z3;
+  h_zipper(h.v1[2], h.v1[3], z2, z3);
+  h.v0[2] += z2;
+  h.v0[3] += z3;
+  h_zipper(h.v0[2], h.v0[3], z2, z3);
+  h.v1[2] += z2;
+  h.v1[3] += z3;
+  p.h = h;
+  return p;
+}
+
 // ==========================================================================
 // extern "C" boundary
 // ==========================================================================
@@ -899,16 +970,8 @@ int lh_highway_prf64(uint64_t start, uint64_t n, const uint64_t key[4], int roun
   int rc = check_device(&sms);
   if (rc) return rc;
   if (n == 0) return LH_OK;
-  Highway h = make_highway(key, 64, rounds);
-  // Length injection for r = 8 (S/highway.py:188-197), key-only.
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t lo = (uint32_t)h.v0[i] + 8u, hi = (uint32_t)(h.v0[i] >> 32) + 8u;
-    h.v0[i] = ((u64)hi << 32) | lo;
-    const uint32_t l1 = (uint32_t)h.v1[i], h1 = (uint32_t)(h.v1[i] >> 32);
-    const uint32_t rl = (l1 << 8) | (l1 >> 24), rh = (h1 << 8) | (h1 >> 24);
-    h.v1[i] = ((u64)rh << 32) | rl;
-  }
-  k_prf<<<grid_for(n, 256, sms), 256, 0, (cudaStream_t)stream>>>(h, start, n, d_out);
+  const PrfProto pp = prf_proto(key, rounds);
+  k_prf<<<grid_for(n, 256, sms), 256, 0, (cudaStream_t)stream>>>(pp, start, n, d_out);
   return cuda_err(cudaGetLastError());
 }
 
