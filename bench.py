@@ -80,10 +80,12 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period: float = 0.05):
+    def __init__(self, index: int, period: float = 0.05, enabled: bool = True):
         self.samples, self.reasons, self.max_mhz = [], 0, None
         self.period, self._stop = period, threading.Event()
         self.ok = False
+        if not enabled:
+            return
         try:
             import pynvml
 
@@ -219,7 +221,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    with ClockSampler(torch.cuda.current_device(), enabled=not args.no_clock_sampler) as clk:
         ev[0].record(stream)
         for i in range(args.steps):
             step()
@@ -277,6 +279,7 @@ def run_ours(args):
                        "parallelism": f"dp{ws} (message-index shards, no collective)",
                        "l2": "inputs 16 GiB per GPU >> 126 MB L2; no flush needed"},
             "msgs_per_s": round(ws * n * args.steps / (total_ms_max / 1e3), 1),
+            **({"steps_ms": [round(x, 3) for x in step_ms]} if args.dump_steps else {}),
             "step_ms": {"min": round(float(np.min(step_ms)), 4),
                         "median": round(float(np.median(step_ms)), 4),
                         "max": round(float(np.max(step_ms)), 4)},
@@ -339,6 +342,8 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clock-sampler", action="store_true")
+    ap.add_argument("--dump-steps", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
