@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
                                                              const uint8_t* __restrict__ buf,
                                                              const u64* __restrict__ offsets,
                                                              const u32* __restrict__ lengths,
-                                                             u64 n, u64* __restrict__ out) {
+                                                             u64 fixed_len, u64 n,
+                                                             u64* __restrict__ out) {
   __shared__ __align__(16) uint4 stage[WARPS][kSpanCap / 16 + 8];
   const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = proto.width / 64;
@@ -179,8 +180,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
     const bool valid = i < n;
     u64 start = 0, len = 0;
     if (valid) {
-      start = offsets[i];
-      len = lengths ? (u64)lengths[i] : offsets[i + 1] - start;
+      if (offsets) {
+        start = offsets[i];
+        len = lengths ? (u64)lengths[i] : offsets[i + 1] - start;
+      } else {  // fixed layout: message i = buf[i*L : (i+1)*L]
+        start = i * fixed_len;
+        len = fixed_len;
+      }
     }
     u64 lo = valid ? start : ~0ull, hi = valid ? start + len : 0;
 #pragma unroll
@@ -899,7 +905,7 @@ int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uin
   const u64 cap = (u64)sms * 8 * (64 / kWarps);
   const u64 blocks = (warps + kWarps - 1) / kWarps;
   k_ragged_short<kWarps><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0,
-                           (cudaStream_t)stream>>>(h, d_buf, d_offsets, d_lengths, n, d_out);
+                           (cudaStream_t)stream>>>(h, d_buf, d_offsets, d_lengths, 0, n, d_out);
   return cuda_err(cudaGetLastError());
 }
 
