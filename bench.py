@@ -267,7 +267,10 @@ def run_ours(args):
         roof["int_pipe"] = {"canonical_ops_per_launch": ops, "peak_ops_per_s": intp["ops_per_s"],
                             "t_int_ms": round(int_t * 1e3, 3),
                             "frac": round(int_t / (per_launch_ms / 1e3), 4),
-                            "source": intp.get("source")}
+                            "peak_source": "measured (profiles/int_peak.json, tools/intpeak.cu)"}
+        read_ceiling = 7260.0  # GB/s, TMA ring with a null consumer (profiles/r1_membench.txt)
+        roof["t_roof_ms"] = round(max(int_t, alg_bytes / (read_ceiling * 1e9)) * 1e3, 3)
+        roof["frac_of_max_hbm_read_or_int"] = round(roof["t_roof_ms"] / per_launch_ms, 4)
 
     result = None
     if rank == 0:
