@@ -773,8 +773,11 @@ bool prefer_split<Highway>(const Highway&, const uint8_t* msgs, u64 n, u64 len) 
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // Few long messages: one thread per message would leave SMs idle.
-  return split_ok(msgs, n, len) && len >= 4096 && n < (u64)sms * 256;
+  // Few long messages: one thread per message would leave SMs idle; and
+  // small-to-medium batches are latency-bound, where halving each thread's
+  // Update chain wins (profiles/README.md: 131,072 x 1 KiB 29 us vs 52 us).
+  return split_ok(msgs, n, len) &&
+         ((len >= 4096 && n < (u64)sms * 256) || (len >= 512 && n < (u64)sms * 1024));
 }
 
 template <class H>
