@@ -45,6 +45,7 @@ def lib():
         l.lh_ref_siptree.argtypes = [vp, vp, u64, i32, i32]
         l.lh_ref_siptree.restype = u64
         l.lh_ref_sip_round.argtypes = [vp]
+        l.lh_ref_zipper_bytes.argtypes = [u64, u64, vp, vp]
         l.lh_ref_hh_update.argtypes = [vp, vp]
         l.lh_ref_hh_init.argtypes = [vp, vp]
         l.lh_ref_hh_remainder_packet.argtypes = [vp, ctypes.c_uint, vp]
