@@ -41,7 +41,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return SO
-    cmd = [NVCC, *FLAGS]
+    cmd = [NVCC, *FLAGS, *os.environ.get("LH_NVCC_EXTRA", "").split()]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     cmd += ["-o", SO] + [os.path.join(CSRC, s) for s in SOURCES]
