@@ -71,29 +71,15 @@ __device__ __forceinline__ void zipper(u64 lo, u64 hi, u64& zlo, u64& zhi) {
   zhi = pack(r2, r3);
 }
 
-// Key-only HighwayHash state (S/highway.py:122-127), expanded on the host and
-// passed by value as a kernel parameter (128 B).
-struct HHState {
-  u64 v0[4], v1[4], m0[4], m1[4];
-};
-
+// The whole per-message HighwayHash state (S/highway.py:43-44, 122-150) plus
+// the finalization parameters.  The key-only initial state is expanded on
+// the host (lh_host.cuh: make_highway) and passed by value as a kernel
+// parameter (the "prototype"); each message starts from a copy of it.
 struct Highway {
   u64 v0[4], v1[4], m0[4], m1[4];
   int rounds;
   int width;  // 64, 128 or 256
   u32 one;    // = 1, opaque to the compiler (see add64_mixed)
-
-  __device__ __forceinline__ void init(const HHState& k, int rounds_, int width_) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v0[i] = k.v0[i];
-      v1[i] = k.v1[i];
-      m0[i] = k.m0[i];
-      m1[i] = k.m1[i];
-    }
-    rounds = rounds_;
-    width = width_;
-  }
 
   // S/highway.py:130-150 — per-lane order of steps 1-5, then the two
   // zipper-merge adds.

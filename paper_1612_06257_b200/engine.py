@@ -253,7 +253,7 @@ def prf64(key, start: int, n: int, rounds: int = 4, out: Optional[torch.Tensor] 
     return out
 
 
-def _one(message) -> torch.Tensor:
+def _one(message):
     device = _require_cuda()
     raw = bytes(message)
     t = torch.frombuffer(bytearray(raw or b"\0"), dtype=torch.uint8)

@@ -126,3 +126,35 @@ def test_prf_2p28(oracle):
     # window invariance over the tail of the range
     t = engine.prf64(synth.key256(), n - 100000, 100000)
     assert torch.equal(t, d[n - 100000:])
+
+
+@pytest.mark.parametrize("cfg", ["128x4", "256x3", "512x3", "128x3", "384x4", "320x5", "448x3"])
+def test_tuning_tile_shapes_are_bit_exact(cfg):
+    """Every LH_TMA_CFG tile shape (tuning knob, read once per process) must
+    produce the same digests as the direct kernel."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import torch\n"
+        "from paper_1612_06257_b200 import engine, synth\n"
+        "from paper_1612_06257_b200.engine import KERNEL_DIRECT, KERNEL_TMA\n"
+        "for n, L in ((200000, 1024), (90001, 48), (70000, 1040)):\n"
+        "    b = torch.empty(n * L, dtype=torch.uint8, device='cuda'); synth.fill_device(b, L)\n"
+        "    m = b.view(n, L)\n"
+        "    for w in (64, 256):\n"
+        "        a = engine.highway_batch(synth.key256(), m, w, kernel=KERNEL_TMA)\n"
+        "        d = engine.highway_batch(synth.key256(), m, w, kernel=KERNEL_DIRECT)\n"
+        "        assert torch.equal(a, d), (n, L, w)\n"
+        "    s = engine.sip_batch(synth.key128(), m, 1, 3, True, kernel=KERNEL_TMA)\n"
+        "    t = engine.sip_batch(synth.key128(), m, 1, 3, True, kernel=KERNEL_DIRECT)\n"
+        "    assert torch.equal(s, t)\n"
+        "print('ok')\n" % ROOT)
+    env = dict(os.environ, LH_TMA_CFG=cfg)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
