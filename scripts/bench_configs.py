@@ -123,6 +123,11 @@ def main():
                             a.steps, a.warmup)
         emit(row("cfg3 short keys 2^26 x U[8,64] (offsets+lengths)", ms, total, n,
                  total + 12 * n + 8 * n, "INT-bound (finalization)"))
+        for name, c, d, tree in (("siphash24", 2, 4, False), ("siphash13", 1, 3, False)):
+            ms, _ = time_launch(lambda: engine.sip_ragged(k128, buf, offs, lens, c, d, tree, out=o),
+                                a.steps, a.warmup)
+            emit(row(f"cfg3-shaped short keys, {name} (ragged)", ms, total, n,
+                     total + 12 * n + 8 * n, "INT-bound"))
         del buf, lens, off, o
         torch.cuda.empty_cache()
 
