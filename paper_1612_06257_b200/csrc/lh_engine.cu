@@ -1,17 +1,27 @@
 // lh_engine.cu — sm_100a kernels and the extern "C" boundary
 // (include/lanehash_b200.h).
 //
-// Kernels (DESIGN.md §Kernels):
+// Kernels (DESIGN.md §3):
 //   k_tma_fixed<H,ROWS,STAGES>  fixed-length batch; one thread per message;
 //       a producer warp streams ROWS x 128-byte boxes of the (n, len) byte
 //       matrix into a STAGES-deep shared-memory ring with 2-D TMA
 //       (SWIZZLE_128B, so each thread's 16-byte reads of its own row are
 //       bank-conflict free); consumer threads run the hash on registers.
+//   k_tma_split  HighwayHash of few long messages: the state split over a
+//       thread pair, 3-D TMA boxes of 16 rows x 512 B per warp.
+//   k_ragged_short  ragged batches of short keys: warp-staged byte spans,
+//       non-divergent Update slots; falls back to the direct reader.
 //   k_direct<H>  any layout (fixed or ragged, any alignment/length); one
 //       thread per message reading its bytes with 8-byte-aligned loads and
 //       funnel shifts.
 //   k_prf        HighwayHash-64 of 8-byte LE counters (no input bytes).
 // H is one of lh::Highway, lh::Sip<C,D>, lh::SipTree<C,D> (lh_device.cuh).
+//
+// Note on hash_direct: keep the reader inline in this shape.  A version
+// split into lh_reader.cuh's absorb_blocks + load_tail made ptxas (CUDA
+// 12.9, sm_100a) rematerialise a loop-carried state word of the
+// finalization loop from the kernel-parameter constant bank -- wrong digests
+// for rounds >= 1.  The parity tests cover rounds 0..5.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
