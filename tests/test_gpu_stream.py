@@ -166,3 +166,17 @@ def test_stream_batch_misuse():
     sb.finish()
     with pytest.raises(RuntimeError):
         sb.append(np.zeros((4, 8), np.uint8))
+
+
+@pytest.mark.parametrize("rounds", [0, 1, 2, 3, 5])
+def test_stream_finalization_rounds(oracle, rounds):
+    """Every kernel is checked at several round counts (a ptxas miscompile
+    once showed only for rounds >= 1)."""
+    n, L = 257, 100
+    data = synth.counter_bytes(500 + rounds, n * L).reshape(n, L)
+    sb = engine.StreamBatch(ALG_HIGHWAY, synth.key256(), n, width=256, rounds=rounds)
+    sb.append(data[:, :37])
+    sb.append(data[:, 37:])
+    got = to_u64(sb.finish())
+    assert np.array_equal(got, oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), data,
+                                                  256, rounds))
