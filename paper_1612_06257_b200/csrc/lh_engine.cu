@@ -207,7 +207,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
     }
     const u32 maxlen = __reduce_max_sync(0xffffffffu, (u32)(len > 0xffffffffull ? 0xffffffffu : len));
     if (maxlen <= 64 && hi - lo <= kSpanCap) {
-      const u64 lo_al = lo & ~15ull, hi_al = (hi + 15) & ~15ull;
+      // Align on the absolute address: d_buf itself need not be 16-B aligned.
+      const u64 base = (u64)(uintptr_t)buf;
+      const u64 lo_al = ((base + lo) & ~15ull) - base, hi_al = ((base + hi + 15) & ~15ull) - base;
       const u32 nch = (u32)((hi_al - lo_al) >> 4);
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
       for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);

@@ -181,9 +181,98 @@ def _to_device(x, dtype, device):
     ).to(device).contiguous()
 
 
+def _launch_ragged(kind, key, buf_ptr, off_ptr, len_ptr, n, p1, p2, tree, out, device):
+    st = _stream_ptr(device)
+    if kind == "hh":
+        rc = _lib.lib().lh_highway_ragged(buf_ptr, off_ptr, len_ptr, n, _key4(key), p1, p2,
+                                          out.data_ptr(), st)
+    else:
+        rc = _lib.lib().lh_siphash_ragged(buf_ptr, off_ptr, len_ptr, n, _key2(key), p1, p2,
+                                          tree, out.data_ptr(), st)
+    _lib.check(rc, "ragged batch")
+
+
+def _host_np(x, dtype):
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        x = x.numpy()
+    return np.ascontiguousarray(x).view(dtype)
+
+
+def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device):
+    """Host ragged batch streamed through the GPU in message-range chunks of
+    about HOST_CHUNK_BYTES: per chunk, the chunk's byte span, its offsets and
+    lengths go H2D, the kernel runs, digests come back D2H, alternating two
+    streams so copies overlap the other chunk's kernel.  Offsets are not
+    rebased: the kernel is handed d_span - span_start as its buffer base, so
+    buf + offsets[i] lands inside the copied span (span_start is 16-aligned,
+    keeping the base 16-aligned).  Returns None when the offsets are too
+    scattered for contiguous spans (caller falls back to one big copy)."""
+    buf = _host_np(buf, np.uint8).reshape(-1)
+    off = _host_np(offsets, np.uint64)
+    lens = _host_np(lengths, np.uint32)
+    n = len(off) - 1 if lens is None else len(off)
+    if n <= 0:
+        return None
+    starts = off[:n]
+    ends = off[1:] if lens is None else off + lens.astype(np.uint64)
+    sizes = (ends - starts).astype(np.int64)
+    csum = np.cumsum(sizes)
+    cuts = [0]
+    while cuts[-1] < n:
+        tgt = (csum[cuts[-1] - 1] if cuts[-1] else 0) + HOST_CHUNK_BYTES
+        nxt = int(np.searchsorted(csum, tgt, side="right"))
+        cuts.append(max(nxt, cuts[-1] + 1) if nxt < n else n)
+    spans = []
+    for a, b in zip(cuts, cuts[1:]):
+        lo = int(starts[a:b].min()) & ~15
+        hi = int(ends[a:b].max())
+        if hi - lo > 4 * max(HOST_CHUNK_BYTES, int(sizes[a:b].sum())):
+            return None  # scattered offsets: no contiguous span per chunk
+        spans.append((a, b, lo, hi))
+    out_host = torch.empty(_out_shape(n, lanes), dtype=torch.int64,
+                           pin_memory=torch.cuda.is_available())
+    buf_t = torch.from_numpy(buf)
+    off_t = torch.from_numpy(off.view(np.int64))
+    len_t = None if lens is None else torch.from_numpy(lens.view(np.int32))
+    streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
+    cur = torch.cuda.current_stream(device)
+    for s in streams:
+        s.wait_stream(cur)
+    keep = []
+    for k, (a, b, lo, hi) in enumerate(spans):
+        s = streams[k % 2]
+        with torch.cuda.stream(s):
+            d_span = buf_t[lo:hi].to(device, non_blocking=True) if hi > lo else \
+                torch.empty(16, dtype=torch.uint8, device=device)
+            if len_t is None:
+                d_off = off_t[a:b + 1].to(device, non_blocking=True)
+                d_len = None
+            else:
+                d_off = off_t[a:b].to(device, non_blocking=True)
+                d_len = len_t[a:b].to(device, non_blocking=True)
+            d_out = torch.empty(_out_shape(b - a, lanes), dtype=torch.int64, device=device)
+            _launch_ragged(kind, key, (d_span.data_ptr() - lo) & 0xFFFFFFFFFFFFFFFF, d_off.data_ptr(),
+                           None if d_len is None else d_len.data_ptr(), b - a, p1, p2, tree,
+                           d_out, device)
+            out_host[a:b].copy_(d_out, non_blocking=True)
+            keep.append((d_span, d_off, d_len, d_out))
+            if len(keep) > 4:
+                keep.pop(0)
+    for s in streams:
+        s.synchronize()
+    return to_u64(out_host)
+
+
 def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None):
     device = _require_cuda()
     host = not (isinstance(buf, torch.Tensor) and buf.is_cuda)
+    if host and out is None and not any(isinstance(x, torch.Tensor) and x.is_cuda
+                                        for x in (offsets, lengths)):
+        r = _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device)
+        if r is not None:
+            return r
     if isinstance(offsets, np.ndarray):
         offsets = offsets.astype(np.uint64, copy=False).view(np.int64)
     if isinstance(lengths, np.ndarray):
@@ -201,16 +290,9 @@ def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None):
     if out is None:
         out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=device)
     if n:
-        st = _stream_ptr(device)
         bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
         lp = d_len.data_ptr() if d_len is not None else None
-        if kind == "hh":
-            rc = _lib.lib().lh_highway_ragged(bp, d_off.data_ptr(), lp, n, _key4(key), p1, p2,
-                                              out.data_ptr(), st)
-        else:
-            rc = _lib.lib().lh_siphash_ragged(bp, d_off.data_ptr(), lp, n, _key2(key), p1, p2,
-                                              tree, out.data_ptr(), st)
-        _lib.check(rc, "ragged batch")
+        _launch_ragged(kind, key, bp, d_off.data_ptr(), lp, n, p1, p2, tree, out, device)
     if host:
         return to_u64(out)
     return out

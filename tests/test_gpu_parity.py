@@ -344,3 +344,58 @@ def test_ragged_short_paths(oracle, case):
     got = engine.highway_ragged(synth.key256(), buf, off, lens, 64, rounds=2)
     want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, lens, 64, 2)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("shift", [1, 3, 8, 13])
+def test_ragged_unaligned_device_buffer(oracle, shift):
+    """d_buf need not be aligned: the warp-staged kernel aligns on the absolute
+    address."""
+    rng = np.random.default_rng(shift)
+    n = 5000
+    lens = rng.integers(0, 65, n).astype(np.uint32)
+    off = np.zeros(n, np.uint64)
+    off[1:] = np.cumsum(lens[:-1])
+    raw = synth.counter_bytes(70 + shift, int(lens.sum()) + 64)
+    d_raw = dev(raw)
+    d_buf = d_raw[shift:]
+    buf = raw[shift:]
+    got = to_u64(engine.highway_ragged(synth.key256(), d_buf, dev(off.view(np.int64)),
+                                       dev(lens.view(np.int32)), 256))
+    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, lens, 256, 4)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("form", ["offsets_n1", "offsets_lengths", "scattered"])
+def test_ragged_host_pipelined_chunks(oracle, form):
+    """Host ragged batches stream through the GPU in message-range chunks;
+    force many small chunks and compare with the oracle."""
+    rng = np.random.default_rng(11)
+    n = 30000
+    lens = rng.integers(0, 300, n).astype(np.uint32)
+    if form == "scattered":
+        off = rng.integers(0, 2_000_000, n).astype(np.uint64)
+        buf = synth.counter_bytes(90, 2_000_400)
+    else:
+        off = np.zeros(n + 1, np.uint64)
+        off[1:] = np.cumsum(lens)
+        buf = synth.counter_bytes(91, int(off[-1]) + 7)
+    old = engine.HOST_CHUNK_BYTES
+    engine.HOST_CHUNK_BYTES = 100_000
+    try:
+        for width in (64, 256):
+            if form == "offsets_n1":
+                got = engine.highway_ragged(synth.key256(), buf, off, None, width)
+                want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, None,
+                                           width, 4)
+            else:
+                o = off[:n]
+                got = engine.highway_ragged(synth.key256(), buf, o, lens, width)
+                want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, o, lens,
+                                           width, 4)
+            assert np.array_equal(got, want), (form, width)
+        o = off[:n]
+        got = engine.sip_ragged(synth.key128(), buf, o, lens, 2, 4, tree=True)
+        assert np.array_equal(got, oracle.batch_ragged(oracle.ALG_SIPTREE, synth.key128(), buf,
+                                                       o, lens, 2, 4))
+    finally:
+        engine.HOST_CHUNK_BYTES = old
