@@ -192,74 +192,65 @@ def _launch_ragged(kind, key, buf_ptr, off_ptr, len_ptr, n, p1, p2, tree, out, d
     _lib.check(rc, "ragged batch")
 
 
-def _host_np(x, dtype):
-    if x is None:
-        return None
-    if isinstance(x, torch.Tensor):
-        x = x.numpy()
-    return np.ascontiguousarray(x).view(dtype)
-
-
 def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device):
     """Host ragged batch streamed through the GPU in message-range chunks of
-    about HOST_CHUNK_BYTES: per chunk, the chunk's byte span, its offsets and
-    lengths go H2D, the kernel runs, digests come back D2H, alternating two
+    about HOST_CHUNK_BYTES.  The offsets/lengths go to the device first (one
+    copy each); each chunk's byte span [min start, max end) is reduced on the
+    device and read back once for all chunks; then per chunk the span goes
+    H2D, the kernel runs and the digests come back D2H, alternating two
     streams so copies overlap the other chunk's kernel.  Offsets are not
-    rebased: the kernel is handed d_span - span_start as its buffer base, so
-    buf + offsets[i] lands inside the copied span (span_start is 16-aligned,
-    keeping the base 16-aligned).  Returns None when the offsets are too
-    scattered for contiguous spans (caller falls back to one big copy)."""
-    buf = _host_np(buf, np.uint8).reshape(-1)
-    off = _host_np(offsets, np.uint64)
-    lens = _host_np(lengths, np.uint32)
-    n = len(off) - 1 if lens is None else len(off)
-    if n <= 0:
+    rebased: the kernel gets d_span - span_start as its buffer base (span_start
+    16-aligned), so buf + offsets[i] lands inside the copied span.  Returns
+    None when the spans are too scattered (caller falls back to one copy)."""
+    buf_t = buf if isinstance(buf, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(buf, dtype=np.uint8))
+    buf_t = buf_t.reshape(-1)
+    off_t = offsets if isinstance(offsets, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(offsets).astype(np.uint64, copy=False).view(np.int64))
+    len_t = None
+    if lengths is not None:
+        len_t = lengths if isinstance(lengths, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(lengths).astype(np.uint32, copy=False).view(np.int32))
+    n = off_t.numel() - 1 if len_t is None else off_t.numel()
+    if n <= 0 or (len_t is not None and len_t.numel() != n):
         return None
-    starts = off[:n]
-    ends = off[1:] if lens is None else off + lens.astype(np.uint64)
-    sizes = (ends - starts).astype(np.int64)
-    csum = np.cumsum(sizes)
-    cuts = [0]
-    while cuts[-1] < n:
-        tgt = (csum[cuts[-1] - 1] if cuts[-1] else 0) + HOST_CHUNK_BYTES
-        nxt = int(np.searchsorted(csum, tgt, side="right"))
-        cuts.append(max(nxt, cuts[-1] + 1) if nxt < n else n)
+    d_off = off_t.to(device, non_blocking=True).contiguous()
+    d_len = None if len_t is None else len_t.to(device, non_blocking=True).contiguous()
+    starts = d_off[:n]
+    ends = d_off[1:] if d_len is None else d_off + d_len.to(torch.int64)
+    # Packed batches: total ~ last end - first start (O(1)); the span check
+    # below catches anything else.
+    est = int(ends[-1].item() - starts[0].item())
+    nchunks = max(1, min(256, -(-max(est, 1) // HOST_CHUNK_BYTES)))
+    cnt = -(-n // nchunks)
+    bounds = [(a, min(n, a + cnt)) for a in range(0, n, cnt)]
+    los = torch.stack([starts[a:b].min() for a, b in bounds])
+    his = torch.stack([ends[a:b].max() for a, b in bounds])
+    los, his = los.cpu().tolist(), his.cpu().tolist()
     spans = []
-    for a, b in zip(cuts, cuts[1:]):
-        lo = int(starts[a:b].min()) & ~15
-        hi = int(ends[a:b].max())
-        if hi - lo > 4 * max(HOST_CHUNK_BYTES, int(sizes[a:b].sum())):
-            return None  # scattered offsets: no contiguous span per chunk
-        spans.append((a, b, lo, hi))
+    for (a, b), lo, hi in zip(bounds, los, his):
+        lo &= ~15
+        if hi - lo > 4 * HOST_CHUNK_BYTES + 4096:
+            return None  # scattered offsets: no compact span per chunk
+        spans.append((a, b, lo, max(hi, lo)))
     out_host = torch.empty(_out_shape(n, lanes), dtype=torch.int64,
                            pin_memory=torch.cuda.is_available())
-    buf_t = torch.from_numpy(buf)
-    off_t = torch.from_numpy(off.view(np.int64))
-    len_t = None if lens is None else torch.from_numpy(lens.view(np.int32))
     streams = [torch.cuda.Stream(device), torch.cuda.Stream(device)]
     cur = torch.cuda.current_stream(device)
     for s in streams:
         s.wait_stream(cur)
-    keep = []
     for k, (a, b, lo, hi) in enumerate(spans):
         s = streams[k % 2]
         with torch.cuda.stream(s):
             d_span = buf_t[lo:hi].to(device, non_blocking=True) if hi > lo else \
                 torch.empty(16, dtype=torch.uint8, device=device)
-            if len_t is None:
-                d_off = off_t[a:b + 1].to(device, non_blocking=True)
-                d_len = None
-            else:
-                d_off = off_t[a:b].to(device, non_blocking=True)
-                d_len = len_t[a:b].to(device, non_blocking=True)
+            d_o = d_off[a:b + 1] if d_len is None else d_off[a:b]
+            d_l = None if d_len is None else d_len[a:b]
             d_out = torch.empty(_out_shape(b - a, lanes), dtype=torch.int64, device=device)
-            _launch_ragged(kind, key, (d_span.data_ptr() - lo) & 0xFFFFFFFFFFFFFFFF, d_off.data_ptr(),
-                           None if d_len is None else d_len.data_ptr(), b - a, p1, p2, tree,
-                           d_out, device)
+            _launch_ragged(kind, key, (d_span.data_ptr() - lo) & 0xFFFFFFFFFFFFFFFF,
+                           d_o.data_ptr(), None if d_l is None else d_l.data_ptr(), b - a,
+                           p1, p2, tree, d_out, device)
             out_host[a:b].copy_(d_out, non_blocking=True)
-            keep.append((d_span, d_off, d_len, d_out))
-            if len(keep) > 4:
-                keep.pop(0)
     for s in streams:
         s.synchronize()
     return to_u64(out_host)
