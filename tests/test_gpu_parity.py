@@ -399,3 +399,25 @@ def test_ragged_host_pipelined_chunks(oracle, form):
                                                        o, lens, 2, 4))
     finally:
         engine.HOST_CHUNK_BYTES = old
+
+
+def test_multi_device_host_batches(oracle):
+    """multi.py: shards on several devices in threads (here the one GPU,
+    listed twice and three times: shards run concurrently on it)."""
+    from paper_1612_06257_b200 import multi
+
+    key = synth.key256()
+    msgs = synth.counter_bytes(41, 3001 * 1024).reshape(3001, 1024)
+    want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, msgs, 256, 4)
+    for devs in ([0], [0, 0], [0, 0, 0]):
+        assert np.array_equal(multi.highway_batch(key, msgs, 256, devices=devs), want), devs
+    got = multi.sip_batch(synth.key128(), msgs, 1, 3, True, devices=[0, 0])
+    assert np.array_equal(got, oracle.batch_fixed(oracle.ALG_SIPTREE, synth.key128(), msgs, 1, 3))
+    lens = synth.lengths(5, 20000, 0, 200)
+    off = np.zeros(20001, np.uint64)
+    off[1:] = np.cumsum(lens)
+    buf = synth.counter_bytes(42, int(off[-1]))
+    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, key, buf, off, None, 64, 4)
+    assert np.array_equal(multi.highway_ragged(key, buf, off, None, 64, devices=[0, 0]), want)
+    assert np.array_equal(multi.highway_ragged(key, buf, off[:-1], lens, 64, devices=[0, 0, 0]),
+                          want)
