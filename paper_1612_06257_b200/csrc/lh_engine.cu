@@ -50,7 +50,10 @@ __host__ __device__ inline int nout<Highway>(const Highway& h) {
   return h.width / 64;
 }
 
-template <class H>
+// PF: prefetch the next packet while hashing the current one (worth it for
+// messages of several packets; costs registers, so fixed batches of short
+// messages use PF = false).
+template <bool PF, class H>
 __device__ __forceinline__ void hash_direct(H& h, const uint8_t* msg, u64 len, u64* out) {
   const u64 full = len & ~31ull;
   const u32 r = (u32)(len & 31);
@@ -58,17 +61,33 @@ __device__ __forceinline__ void hash_direct(H& h, const uint8_t* msg, u64 len, u
   const u32 sh = (u32)(a & 7) * 8;
   const u64* w = (const u64*)(a & ~(uintptr_t)7);
   u64 t[4] = {0, 0, 0, 0};
+  const u64 nb = full >> 5;
   if (sh == 0) {
     if ((a & 15) == 0) {
+      // Next packet's loads are issued before this packet's Update (one
+      // thread walks its message alone; hide the load latency in-thread).
       const ulonglong2* w2 = (const ulonglong2*)w;
-      for (u64 b = 0; b < (full >> 5); ++b) {
-        const ulonglong2 x = __ldg(w2 + 2 * b);
-        const ulonglong2 y = __ldg(w2 + 2 * b + 1);
+      ulonglong2 x = {0, 0}, y = {0, 0};
+      if (PF && nb) {
+        x = __ldg(w2);
+        y = __ldg(w2 + 1);
+      }
+      for (u64 b = 0; b < nb; ++b) {
+        ulonglong2 xn = {0, 0}, yn = {0, 0};
+        if (!PF) {
+          x = __ldg(w2 + 2 * b);
+          y = __ldg(w2 + 2 * b + 1);
+        } else if (b + 1 < nb) {
+          xn = __ldg(w2 + 2 * b + 2);
+          yn = __ldg(w2 + 2 * b + 3);
+        }
         const u64 p[4] = {x.x, x.y, y.x, y.y};
         h.absorb32(p);
+        x = xn;
+        y = yn;
       }
     } else {
-      for (u64 b = 0; b < (full >> 5); ++b) {
+      for (u64 b = 0; b < nb; ++b) {
         const u64 p[4] = {ldg64(w + 4 * b), ldg64(w + 4 * b + 1), ldg64(w + 4 * b + 2),
                           ldg64(w + 4 * b + 3)};
         h.absorb32(p);
@@ -84,13 +103,36 @@ __device__ __forceinline__ void hash_direct(H& h, const uint8_t* msg, u64 len, u
     }
   } else {
     u64 cur = len ? ldg64(w) : 0;
-    for (u64 b = 0; b < (full >> 5); ++b) {
-      const u64* q = w + 4 * b;
-      const u64 n0 = ldg64(q + 1), n1 = ldg64(q + 2), n2 = ldg64(q + 3), n3 = ldg64(q + 4);
+    u64 n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+    if (PF && nb) {
+      n0 = ldg64(w + 1);
+      n1 = ldg64(w + 2);
+      n2 = ldg64(w + 3);
+      n3 = ldg64(w + 4);
+    }
+    for (u64 b = 0; b < nb; ++b) {
+      u64 m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+      if (!PF) {
+        const u64* q = w + 4 * b;
+        n0 = ldg64(q + 1);
+        n1 = ldg64(q + 2);
+        n2 = ldg64(q + 3);
+        n3 = ldg64(q + 4);
+      } else if (b + 1 < nb) {  // prefetch the next packet's words
+        const u64* q = w + 4 * b + 4;
+        m0 = ldg64(q + 1);
+        m1 = ldg64(q + 2);
+        m2 = ldg64(q + 3);
+        m3 = ldg64(q + 4);
+      }
       const u64 p[4] = {funnel(cur, n0, sh), funnel(n0, n1, sh), funnel(n1, n2, sh),
                         funnel(n2, n3, sh)};
       cur = n3;
       h.absorb32(p);
+      n0 = m0;
+      n1 = m1;
+      n2 = m2;
+      n3 = m3;
     }
     if (r) {
       // words covering [a+full, a+full+r): cur plus `extra` more.
@@ -109,7 +151,7 @@ __device__ __forceinline__ void hash_direct(H& h, const uint8_t* msg, u64 len, u
   h.finish(t, r, len, out);
 }
 
-template <class H>
+template <class H, bool PF>
 __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __restrict__ buf,
                                                 const u64* __restrict__ offsets,
                                                 const u32* __restrict__ lengths, u64 fixed_len,
@@ -128,7 +170,7 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
       len = fixed_len;
     }
     H h = proto;
-    hash_direct(h, msg, len, out + i * W);
+    hash_direct<PF>(h, msg, len, out + i * W);
   }
 }
 
@@ -260,7 +302,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       __syncwarp();
     } else if (valid) {
       Highway h = proto;
-      hash_direct(h, buf + start, len, out + i * W);
+      hash_direct<true>(h, buf + start, len, out + i * W);
     }
   }
 }
@@ -621,8 +663,12 @@ int launch_direct(const H& proto, const uint8_t* buf, const u64* offsets, const 
   int rc = check_device(&sms);
   if (rc) return rc;
   if (n == 0) return LH_OK;
-  k_direct<H><<<grid_for(n, 256, sms), 256, 0, st>>>(proto, buf, offsets, lengths, fixed_len,
-                                                     n, out);
+  if (offsets || fixed_len >= 64)
+    k_direct<H, true><<<grid_for(n, 256, sms), 256, 0, st>>>(proto, buf, offsets, lengths,
+                                                             fixed_len, n, out);
+  else
+    k_direct<H, false><<<grid_for(n, 256, sms), 256, 0, st>>>(proto, buf, offsets, lengths,
+                                                              fixed_len, n, out);
   return cuda_err(cudaGetLastError());
 }
 
