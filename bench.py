@@ -170,13 +170,38 @@ def cpu_baseline(steps: int, warmup: int = 1, nthreads=None, min_seconds: float 
         times.append(time.perf_counter() - t0)
     total = sum(times)
     gbs = len(times) * CPU_SAMPLE_MSGS * MSG_BYTES / total / 1e9
+    # One core on a smaller slice, for the per-core figure SURVEY.md §8d asks for.
+    one = msgs[:CPU_SAMPLE_MSGS // 8]
+    t1, n1 = 0.0, 0
+    while t1 < 1.0:
+        t0 = time.perf_counter()
+        orc.batch_fixed(orc.ALG_HIGHWAY, key, one, 64, 4, nthreads=1)
+        t1 += time.perf_counter() - t0
+        n1 += 1
     return {
         "value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
         "sample": f"{len(times)} passes x {CPU_SAMPLE_MSGS} msgs x {MSG_BYTES} B "
                   f"(first messages of the bench batch), oracle/lh_oracle.c, {threads} threads, "
                   f"{total:.2f} s",
         "seconds": total,
+        "single_core": {"value": round(n1 * one.nbytes / t1 / 1e9, 3), "unit": UNIT,
+                        "sample": f"{n1} passes x {len(one)} msgs, 1 thread, {t1:.2f} s"},
+        "host": _host_info(),
     }
+
+
+def _host_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0))}
 
 
 def len_or(k):
@@ -198,7 +223,8 @@ def run_reference(args):
         "config": {"workload": f"hh64 over {CPU_SAMPLE_MSGS} x 1 KiB per step (bounded sample of "
                                f"the 2^24 x 1 KiB batch)", "messages_per_step": CPU_SAMPLE_MSGS,
                    "msg_bytes": MSG_BYTES, "digest_bits": 64},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                             "single_core", "host")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -272,7 +298,9 @@ def run_ours(args):
             "frac": round(achieved / peak, 4), "traffic": _traffic(),
             "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
-            "kernel": "k_tma_fixed<Highway,512,3,1>"}
+            "kernel": "k_tma_fixed<Highway,512,3,1>",
+            # north_star's nominal 8.0 TB/s HBM figure, reported beside the measured peak
+            "frac_of_nominal_8000": round(achieved / 8000.0, 4)}
     intp = _int_peak()
     if intp and intp.get("ops_per_s"):
         ops = (80 * (L // 32 + 4) + 4) * n
