@@ -135,6 +135,23 @@ int lh_avalanche_counts(int alg, const uint64_t* key, const uint8_t* d_msgs,
                         uint64_t iters, uint32_t size, int p1, int p2,
                         int64_t* d_counts, void* stream);
 
+/* ---- Raw Update and its inverse (test / self-test entries) ----
+ * Replaces: update (S/highway.py:130-150) and update_inverse
+ * (S/highway.py:153-173), which the reference uses as the bijectivity
+ * oracle of T/test_update.py:56-67 and T/test_acceptance.py:42-63.
+ * d_states: n x 16 u64 (v0[4], v1[4], mul0[4], mul1[4]), updated in place;
+ * d_packets: n x 4 u64.  inverse: 0 = update, 1 = update_inverse.  The
+ * device code is the Update every hashing kernel inlines. */
+int lh_highway_update_states(uint64_t* d_states, const uint64_t* d_packets,
+                             uint64_t n, int inverse, void* stream);
+/* Device self-test of the bijection on n synthetic cases: case i is words
+ * 20i .. 20i+19 of the synthetic stream (seed, stream_id 0) -- 16 state
+ * lanes, then 4 packet lanes.  ACCUMULATES (caller zeroes d_result[0..1]):
+ * d_result[0] += #cases with update_inverse(update(s)) != s,
+ * d_result[1] ^= XOR of all 16 lanes of update(s) over the cases. */
+int lh_highway_bijectivity(uint64_t seed, uint64_t n, uint64_t* d_result,
+                           void* stream);
+
 /* Seeded synthetic input generator (bench/test harness; not a reference
  * interface).  Byte b of the stream is byte (b & 7) of
  * word(seed, stream_id, word_offset + b / 8), see DESIGN.md §Synthetic

@@ -47,6 +47,8 @@ def lib():
         l.lh_ref_sip_round.argtypes = [vp]
         l.lh_ref_zipper_bytes.argtypes = [u64, u64, vp, vp]
         l.lh_ref_hh_update.argtypes = [vp, vp]
+        l.lh_ref_hh_update_inverse.argtypes = [vp, vp]
+        l.lh_ref_update_states.argtypes = [vp, vp, u64, i32]
         l.lh_ref_hh_init.argtypes = [vp, vp]
         l.lh_ref_hh_remainder_packet.argtypes = [vp, ctypes.c_uint, vp]
         l.lh_ref_avalanche_counts.argtypes = [i32, vp, vp, u64, ctypes.c_uint32, i32, i32, vp, i32]
@@ -120,6 +122,18 @@ def batch_ragged(alg, key, buf: np.ndarray, offsets: np.ndarray, lengths=None,
                               n, p1, p2, _ptr(out), _threads(nthreads))
     out = out[: n * w]
     return out.reshape(n, w) if w > 1 else out
+
+
+def update_states(states: np.ndarray, packets: np.ndarray, inverse: bool = False) -> np.ndarray:
+    """S/highway.py:130-173 on n raw states: (n,16) uint64 (v0, v1, mul0,
+    mul1 lanes) and (n,4) uint64 packets; returns the new states."""
+    st = np.array(states, dtype=np.uint64, order="C", copy=True).reshape(-1, 16)
+    pk = np.ascontiguousarray(packets, dtype=np.uint64).reshape(-1, 4)
+    if len(st) != len(pk):
+        raise ValueError("states and packets differ in length")
+    if len(st):
+        lib().lh_ref_update_states(_ptr(st), _ptr(pk), len(st), int(bool(inverse)))
+    return st
 
 
 def prf64(key, start: int, n: int, rounds: int = 4, nthreads=None) -> np.ndarray:

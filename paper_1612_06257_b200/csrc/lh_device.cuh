@@ -111,6 +111,31 @@ struct Highway {
     update(p[0], p[1], p[2], p[3]);
   }
 
+  // S/highway.py:153-173: the exact inverse of update for the same packet
+  // (self-test only; never on a hashing path).
+  __device__ __forceinline__ void update_inverse(const u64 (&p)[4]) {
+    u64 z0, z1, z2, z3;
+    zipper(v0[0], v0[1], z0, z1);
+    zipper(v0[2], v0[3], z2, z3);
+    v1[0] -= z0;
+    v1[1] -= z1;
+    v1[2] -= z2;
+    v1[3] -= z3;
+    zipper(v1[0], v1[1], z0, z1);
+    zipper(v1[2], v1[3], z2, z3);
+    v0[0] -= z0;
+    v0[1] -= z1;
+    v0[2] -= z2;
+    v0[3] -= z3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      m1[i] ^= mul_lo_hi(v0[i], v1[i]);
+      v0[i] -= m1[i];
+      m0[i] ^= mul_lo_hi(v1[i], v0[i]);
+      v1[i] -= p[i] + m0[i];
+    }
+  }
+
   // S/highway.py:182-220.  t holds the r tail bytes (zero beyond r).
   __device__ __forceinline__ void remainder(const u64 (&t)[4], u32 r) {
 #pragma unroll

@@ -1,0 +1,138 @@
+// lh_state.cu — the raw HighwayHash Update and its inverse on caller states,
+// and a device self-test of the bijection.
+//
+//   update         S/highway.py:130-150  (lh::Highway::update, the hot-path code)
+//   update_inverse S/highway.py:153-173  (lh::Highway::update_inverse)
+//
+// The reference uses update_inverse only as a test oracle: the permutation
+// check of T/test_update.py:56-67 and the acceptance gate
+// T/test_acceptance.py:42-63 (100,000 round trips in < 5 s).  Here the same
+// check runs on the device over any number of synthetic states, through the
+// exact Update the hashing kernels inline.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lanehash_b200.h"
+#include "lh_device.cuh"
+#include "lh_mix.cuh"
+
+using namespace lh;
+
+namespace {
+
+__device__ __forceinline__ void load_state(Highway& h, const u64* s) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h.v0[i] = s[i];
+    h.v1[i] = s[4 + i];
+    h.m0[i] = s[8 + i];
+    h.m1[i] = s[12 + i];
+  }
+}
+
+__device__ __forceinline__ void store_state(const Highway& h, u64* s) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    s[i] = h.v0[i];
+    s[4 + i] = h.v1[i];
+    s[8 + i] = h.m0[i];
+    s[12 + i] = h.m1[i];
+  }
+}
+
+template <bool INV>
+__global__ void k_update_states(u64* __restrict__ states, const u64* __restrict__ packets, u64 n,
+                                u32 one) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    Highway h;
+    h.one = one;
+    load_state(h, states + 16 * i);
+    const u64 p[4] = {packets[4 * i], packets[4 * i + 1], packets[4 * i + 2], packets[4 * i + 3]};
+    if (INV)
+      h.update_inverse(p);
+    else
+      h.update(p[0], p[1], p[2], p[3]);
+    store_state(h, states + 16 * i);
+  }
+}
+
+// Case i = words 20i .. 20i+19 of the synthetic stream: 16 state lanes, then
+// 4 packet lanes.  result[0] += failures, result[1] ^= fold of update(s).
+__global__ void k_bijectivity(u64 key, u64 n, u32 one, unsigned long long* result) {
+  u64 fails = 0, fold = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    u64 s[16], p[4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s[j] = synth_word(key, 20 * i + j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) p[j] = synth_word(key, 20 * i + 16 + j);
+    Highway h;
+    h.one = one;
+    load_state(h, s);
+    h.update(p[0], p[1], p[2], p[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fold ^= h.v0[j] ^ h.v1[j] ^ h.m0[j] ^ h.m1[j];
+    h.update_inverse(p);
+    u64 diff = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      diff |= (h.v0[j] ^ s[j]) | (h.v1[j] ^ s[4 + j]) | (h.m0[j] ^ s[8 + j]) | (h.m1[j] ^ s[12 + j]);
+    fails += diff != 0;
+  }
+  // Warp-reduce, then one atomic per warp.
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fails += __shfl_xor_sync(0xffffffffu, fails, o);
+    fold ^= __shfl_xor_sync(0xffffffffu, fold, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (fails) atomicAdd(&result[0], (unsigned long long)fails);
+    atomicXor(&result[1], (unsigned long long)fold);
+  }
+}
+
+unsigned grid_for(u64 items, int sms) {
+  const u64 b = (items + 255) / 256;
+  const u64 cap = (u64)sms * 8;
+  return (unsigned)(b == 0 ? 1 : (b > cap ? cap : b));
+}
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lh_highway_update_states(uint64_t* d_states, const uint64_t* d_packets, uint64_t n,
+                             int inverse, void* stream) {
+  if (n && (!d_states || !d_packets)) return LH_EINVAL;
+  if (inverse != 0 && inverse != 1) return LH_EINVAL;
+  if ((uintptr_t)d_states % 8 || (uintptr_t)d_packets % 8) return LH_EALIGN;
+  if (!n) return LH_OK;
+  const unsigned g = grid_for(n, sm_count());
+  cudaStream_t st = (cudaStream_t)stream;
+  if (inverse)
+    k_update_states<true><<<g, 256, 0, st>>>(d_states, d_packets, n, 1u);
+  else
+    k_update_states<false><<<g, 256, 0, st>>>(d_states, d_packets, n, 1u);
+  return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
+}
+
+int lh_highway_bijectivity(uint64_t seed, uint64_t n, uint64_t* d_result, void* stream) {
+  if (!d_result) return LH_EINVAL;
+  if ((uintptr_t)d_result % 8) return LH_EALIGN;
+  if (!n) return LH_OK;
+  const unsigned g = grid_for(n, sm_count());
+  k_bijectivity<<<g, 256, 0, (cudaStream_t)stream>>>(synth_key(seed, 0), n, 1u,
+                                                      (unsigned long long*)d_result);
+  return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
+}
+
+}  // extern "C"

@@ -8,16 +8,12 @@
 #include <stdint.h>
 
 #include "../../include/lanehash_b200.h"
+#include "lh_mix.cuh"
 
 namespace {
 
-constexpr uint64_t kG = 0x9E3779B97F4A7C15ull;
-
-__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
+using lh::kG;
+using lh::mix64;
 
 __global__ void k_fill(uint64_t* __restrict__ dst, uint64_t nwords, uint64_t key,
                        uint64_t word_offset) {

@@ -326,6 +326,49 @@ def prf64(key, start: int, n: int, rounds: int = 4, out: Optional[torch.Tensor] 
     return out
 
 
+def update_states(states, packets, inverse: bool = False):
+    """update (S/highway.py:130-150) or update_inverse (:153-173) of n raw
+    states: (n,16) lanes v0, v1, mul0, mul1 and (n,4) packets, uint64 numpy
+    or int64 CUDA tensors.  CUDA tensors are updated in place and returned;
+    host arrays come back as a new numpy uint64 array."""
+    device = _require_cuda()
+    host = not (isinstance(states, torch.Tensor) and states.is_cuda)
+    if host:
+        st = np.ascontiguousarray(states, dtype=np.uint64).reshape(-1, 16)
+        pk = np.ascontiguousarray(packets, dtype=np.uint64).reshape(-1, 4)
+        d_st = torch.from_numpy(st.view(np.int64).copy()).to(device)
+        d_pk = torch.from_numpy(pk.view(np.int64)).to(device)
+    else:
+        d_st, d_pk = states, packets
+        if not isinstance(d_pk, torch.Tensor) or not d_pk.is_cuda:
+            raise ValueError("states and packets must both be CUDA tensors (or both host)")
+        if d_st.dtype != torch.int64 or d_pk.dtype != torch.int64:
+            raise ValueError("CUDA states and packets must be int64 tensors")
+        if not (d_st.is_contiguous() and d_pk.is_contiguous()):
+            raise ValueError("CUDA states and packets must be contiguous")
+    n = d_st.numel() // 16
+    if d_st.numel() != 16 * n or d_pk.numel() != 4 * n:
+        raise ValueError("need (n,16) states and (n,4) packets")
+    if n:
+        rc = _lib.lib().lh_highway_update_states(d_st.data_ptr(), d_pk.data_ptr(), n,
+                                                 int(bool(inverse)), _stream_ptr(device))
+        _lib.check(rc, "lh_highway_update_states")
+    return to_u64(d_st).reshape(n, 16) if host else d_st
+
+
+def bijectivity(seed: int, n: int):
+    """Device self-test: (failures, fold) over n synthetic (state, packet)
+    cases, case i = words 20i..20i+19 of synth stream (seed, 0)."""
+    device = _require_cuda()
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    res = torch.zeros(2, dtype=torch.int64, device=device)
+    rc = _lib.lib().lh_highway_bijectivity(seed, n, res.data_ptr(), _stream_ptr(device))
+    _lib.check(rc, "lh_highway_bijectivity")
+    r = to_u64(res)
+    return int(r[0]), int(r[1])
+
+
 def _one(message):
     device = _require_cuda()
     raw = bytes(message)

@@ -108,6 +108,45 @@ def hash256(key, message: bytes, rounds: int = 4) -> Tuple[int, int, int, int]:
     return tuple(int(x) for x in out)
 
 
+#: (v0, v1, mul0, mul1), four lanes each (S/highway.py:40).
+State = Tuple[Tuple[int, int, int, int], ...]
+
+
+def _rot32(x: int) -> int:
+    return ((x >> 32) | (x << 32)) & _MASK64
+
+
+def initialize(key) -> State:
+    """Key expansion (S/highway.py:122-127): v0 = k ^ INIT0,
+    v1 = rot32(k) ^ INIT1, mul0 = INIT0, mul1 = INIT1.  Key-only, so it is
+    host logic (the engine expands the key once per batch, lh_host.cuh)."""
+    k = as_key256(key).lanes
+    return (tuple(k[i] ^ INIT0[i] for i in range(4)),
+            tuple(_rot32(k[i]) ^ INIT1[i] for i in range(4)), INIT0, INIT1)
+
+
+def _state_op(state: State, packet: Sequence[int], inverse: bool) -> State:
+    from . import engine
+    import numpy as np
+
+    if len(state) != 4 or any(len(x) != 4 for x in state) or len(packet) != 4:
+        raise ValueError("state is four 4-lane tuples and packet four lanes")
+    st = np.array([[x & _MASK64 for lanes in state for x in lanes]], dtype=np.uint64)
+    pk = np.array([[x & _MASK64 for x in packet]], dtype=np.uint64)
+    out = [int(x) for x in engine.update_states(st, pk, inverse)[0]]
+    return tuple(tuple(out[i:i + 4]) for i in range(0, 16, 4))
+
+
+def update(state: State, packet: Sequence[int]) -> State:
+    """One Update step (S/highway.py:130-150) on the GPU engine."""
+    return _state_op(state, packet, False)
+
+
+def update_inverse(state: State, packet: Sequence[int]) -> State:
+    """Exact inverse of :func:`update` (S/highway.py:153-173) on the GPU."""
+    return _state_op(state, packet, True)
+
+
 class StreamingHasher:
     """Incremental HighwayHash (S/highway.py:257-285) on the GPU engine.
 

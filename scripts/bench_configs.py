@@ -14,6 +14,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 import numpy as np
 import torch
@@ -21,7 +22,10 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+from bench import ClockSampler  # noqa: E402
 from paper_1612_06257_b200 import engine, synth  # noqa: E402
+
+LAST_CLOCKS = {}  # NVML SM clock / throttle reasons of the last timed region
 
 
 def peak_gbs():
@@ -31,17 +35,25 @@ def peak_gbs():
         return 6650.0
 
 
+SETTLE_S = 2.0  # idle before each workload so none inherits the previous one's power-cap state
+
+
 def time_launch(fn, steps, warmup):
+    torch.cuda.synchronize()
+    time.sleep(SETTLE_S)
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-    ev[0].record(st)
-    for i in range(steps):
-        fn()
-        ev[i + 1].record(st)
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device(), period=0.01) as clk:
+        ev[0].record(st)
+        for i in range(steps):
+            fn()
+            ev[i + 1].record(st)
+        torch.cuda.synchronize()
+    LAST_CLOCKS.clear()
+    LAST_CLOCKS.update(clk.summary())
     ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
     return float(np.median(ms)), float(np.min(ms))
 
@@ -53,7 +65,7 @@ def row(name, ms, payload, nmsgs, alg_bytes, note, extra=None):
          "msgs_per_s": round(nmsgs / ms * 1e3, 1),
          "hbm_alg_bytes": alg_bytes,
          "hbm_frac_of_measured_copy": round(alg_bytes / ms / 1e6 / pk, 4),
-         "note": note}
+         "note": note, "clocks": dict(LAST_CLOCKS)}
     if extra:
         r.update(extra)
     return r
@@ -65,7 +77,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--only", default="")
     ap.add_argument("--out", default="")
+    ap.add_argument("--settle", type=float, default=SETTLE_S)
     a = ap.parse_args()
+    globals()["SETTLE_S"] = a.settle
     dev = torch.device("cuda", 0)
     key, k128 = synth.key256(), synth.key128()
     out = []
@@ -165,7 +179,6 @@ def main():
 
     if on("e2e"):
         # End to end from pinned host memory through the public API (H2D, kernel, D2H).
-        import time
         n, L = 1 << 21, 1024
         host = torch.empty((n, L), dtype=torch.uint8, pin_memory=True)
         tmp = torch.empty(n * L, dtype=torch.uint8, device=dev)

@@ -58,6 +58,11 @@ def test_abi_rejects_bad_arguments_before_touching_the_device():
     assert l.lh_highway_fixed(addr(buf), 1 << 40, 1 << 40, key4, 64, 4, addr(out), None) == \
         _lib.LH_ETOOBIG
     assert l.lh_synth_fill(addr(buf) + 1, 8, 0, 0, 0, None) == _lib.LH_EALIGN
+    # raw Update: inverse flag must be 0/1, states 8-byte aligned
+    assert l.lh_highway_update_states(addr(out), addr(out), 1, 2, None) == _lib.LH_EINVAL
+    assert l.lh_highway_update_states(None, addr(out), 1, 0, None) == _lib.LH_EINVAL
+    assert l.lh_highway_update_states(addr(out) + 4, addr(out), 1, 0, None) == _lib.LH_EALIGN
+    assert l.lh_highway_bijectivity(0, 1, None, None) == _lib.LH_EINVAL
 
 
 def test_check_maps_errors_like_the_reference():
@@ -85,6 +90,23 @@ def test_constants_match_reference(golden):
     assert list(lh.ZIPPER_OFFSETS) == golden["zipper_offsets"]
     assert sorted(lh.ZIPPER_OFFSETS) == list(range(16))
     assert bytes(lh.ZIPPER_OFFSETS).hex() == "030c02050e010f000b040a0d09060807"
+
+
+def test_initialize_matches_reference_layout(golden):
+    """S/highway.py:122-127 (host key expansion) against the golden init lanes."""
+    from paper_1612_06257_b200 import highway
+
+    key = bytes(range(32))
+    v0, v1, m0, m1 = highway.initialize(key)
+    lanes = struct.unpack("<4Q", key)
+    rot = lambda x: ((x >> 32) | (x << 32)) & ((1 << 64) - 1)
+    init0 = [int(x, 16) for x in golden["init0"]]
+    init1 = [int(x, 16) for x in golden["init1"]]
+    assert list(v0) == [k ^ c for k, c in zip(lanes, init0)]
+    assert list(v1) == [rot(k) ^ c for k, c in zip(lanes, init1)]
+    assert list(m0) == init0 and list(m1) == init1
+    with pytest.raises(ValueError):
+        highway.update(((0,) * 4,) * 3, (0,) * 4)
 
 
 def test_zipper_prmt_selectors_match_byte_table():
