@@ -111,3 +111,15 @@ def get_algorithm(name: str) -> Algorithm:
         return ALGORITHMS[name]
     except KeyError:
         raise ValueError(f"unknown algorithm: {name!r}") from None
+
+
+def finalization_variant(rounds: int):
+    """HighwayHash-64 with a non-default finalization depth, as a
+    ``(key bytes, message bytes) -> int`` callable (S/registry.py:200-204),
+    through the selected backend."""
+    from .backends import get_backend
+    from .highway import Key256
+
+    if rounds < 0:
+        raise ValueError("rounds must be >= 0")
+    return lambda key, msg: get_backend().hash64(Key256.from_bytes(key), msg, rounds)

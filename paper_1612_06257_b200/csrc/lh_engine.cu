@@ -633,26 +633,28 @@ unsigned grid_for(u64 n, int threads, int sms) {
   return (unsigned)(blocks < cap ? (blocks ? blocks : 1) : cap);
 }
 
+// Process-wide settings are function-local statics initialised once by a
+// lambda (thread-safe under C++11): host threads driving several devices
+// (multi.py) may make their first calls concurrently.
 u32 tma_l2_prefetch() {
-  static int pf = -1;
-  if (pf < 0) {
+  static const u32 pf = [] {
     const char* s = getenv("LH_TMA_PF");
-    pf = s ? atoi(s) : 0;
-    if (pf < 0) pf = 0;
-  }
-  return (u32)pf;
+    const int v = s ? atoi(s) : 0;
+    return (u32)(v < 0 ? 0 : v);
+  }();
+  return pf;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-  }
+      return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -762,20 +764,18 @@ bool split_ok(const uint8_t* msgs, u64 n, u64 len) {
 // Tuning knobs (read once): LH_TMA_CFG=128x4|256x3|512x3|128x3 tile shape,
 // LH_TMA_PF=<boxes> L2 prefetch distance.  Defaults: automatic.
 int tma_cfg_override() {
-  static int cfg = -1;
-  if (cfg < 0) {
+  static const int cfg = [] {
     const char* s = getenv("LH_TMA_CFG");
-    cfg = 0;
-    if (s) {
-      if (!strcmp(s, "128x4")) cfg = 1;
-      else if (!strcmp(s, "256x3")) cfg = 2;
-      else if (!strcmp(s, "512x3")) cfg = 3;
-      else if (!strcmp(s, "384x4")) cfg = 5;
-      else if (!strcmp(s, "320x5")) cfg = 6;
-      else if (!strcmp(s, "448x3")) cfg = 7;
-      else if (!strcmp(s, "128x3")) cfg = 4;
-    }
-  }
+    if (!s) return 0;
+    if (!strcmp(s, "128x4")) return 1;
+    if (!strcmp(s, "256x3")) return 2;
+    if (!strcmp(s, "512x3")) return 3;
+    if (!strcmp(s, "128x3")) return 4;
+    if (!strcmp(s, "384x4")) return 5;
+    if (!strcmp(s, "320x5")) return 6;
+    if (!strcmp(s, "448x3")) return 7;
+    return 0;
+  }();
   return cfg;
 }
 

@@ -70,3 +70,15 @@ def test_exhaustive_finalization_experiment_runs():
     r4 = quality.finalization_bias_experiment(4, exhaustive=True, seed=9)
     assert r3.inputs == r4.inputs == 2**24
     assert 0 < r4.max_bias < r3.max_bias
+
+
+def test_finalization_variant(oracle):
+    """S/registry.py:200-204: hash64 at a chosen finalization depth."""
+    from paper_1612_06257_b200.catalog import finalization_variant
+
+    key = bytes(range(32))
+    lanes = np.frombuffer(key, np.uint64)
+    for r in (0, 1, 3, 4, 6):
+        f = finalization_variant(r)
+        for msg in (b"", b"abc", bytes(range(33))):
+            assert f(key, msg) == oracle.highway(lanes, msg, r)[0]
