@@ -22,6 +22,7 @@ Reference correspondence (S = /root/reference/pkg/src/lanehash):
 from __future__ import annotations
 
 import ctypes
+import warnings
 from typing import Optional
 
 import numpy as np
@@ -65,6 +66,18 @@ def to_u64(t) -> np.ndarray:
     return np.asarray(t).view(np.uint64)
 
 
+def _host_view(a: np.ndarray) -> torch.Tensor:
+    """Zero-copy torch view of a host array the engine only reads.  Read-only
+    arrays (np.frombuffer(bytes), read-only np.memmap) are fine: torch warns
+    that writes through the view would be undefined, and there are none."""
+    a = np.ascontiguousarray(a)
+    if a.flags.writeable:
+        return torch.from_numpy(a)
+    with warnings.catch_warnings():
+        warnings.filterwarnings("ignore", message=".*not writable.*", category=UserWarning)
+        return torch.from_numpy(a)
+
+
 def _as_u8_2d(msgs):
     if isinstance(msgs, torch.Tensor):
         if msgs.dtype != torch.uint8 or msgs.dim() != 2:
@@ -73,10 +86,7 @@ def _as_u8_2d(msgs):
     a = np.asarray(msgs)
     if a.dtype != np.uint8 or a.ndim != 2:
         raise ValueError("messages must be a 2-D uint8 array (n, length)")
-    a = np.ascontiguousarray(a)
-    if not a.flags.writeable:  # e.g. np.frombuffer(bytes): torch wants writable memory
-        a = a.copy()
-    return torch.from_numpy(a)
+    return _host_view(a)
 
 
 def _out_shape(n: int, lanes: int):
@@ -176,7 +186,7 @@ def _to_device(x, dtype, device):
         if x.dtype != dtype:
             raise ValueError(f"expected {dtype}, got {x.dtype}")
         return x.to(device, non_blocking=True).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(x).view(
+    return _host_view(np.ascontiguousarray(x).view(
         {torch.uint8: np.uint8, torch.int64: np.int64, torch.int32: np.int32}[dtype])
     ).to(device).contiguous()
 
@@ -202,14 +212,14 @@ def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes
     rebased: the kernel gets d_span - span_start as its buffer base (span_start
     16-aligned), so buf + offsets[i] lands inside the copied span.  Returns
     None when the spans are too scattered (caller falls back to one copy)."""
-    buf_t = buf if isinstance(buf, torch.Tensor) else torch.from_numpy(
+    buf_t = buf if isinstance(buf, torch.Tensor) else _host_view(
         np.ascontiguousarray(buf, dtype=np.uint8))
     buf_t = buf_t.reshape(-1)
-    off_t = offsets if isinstance(offsets, torch.Tensor) else torch.from_numpy(
+    off_t = offsets if isinstance(offsets, torch.Tensor) else _host_view(
         np.ascontiguousarray(offsets).astype(np.uint64, copy=False).view(np.int64))
     len_t = None
     if lengths is not None:
-        len_t = lengths if isinstance(lengths, torch.Tensor) else torch.from_numpy(
+        len_t = lengths if isinstance(lengths, torch.Tensor) else _host_view(
             np.ascontiguousarray(lengths).astype(np.uint32, copy=False).view(np.int32))
     n = off_t.numel() - 1 if len_t is None else off_t.numel()
     if n <= 0 or (len_t is not None and len_t.numel() != n):
@@ -337,7 +347,7 @@ def update_states(states, packets, inverse: bool = False):
         st = np.ascontiguousarray(states, dtype=np.uint64).reshape(-1, 16)
         pk = np.ascontiguousarray(packets, dtype=np.uint64).reshape(-1, 4)
         d_st = torch.from_numpy(st.view(np.int64).copy()).to(device)
-        d_pk = torch.from_numpy(pk.view(np.int64)).to(device)
+        d_pk = _host_view(pk.view(np.int64)).to(device)
     else:
         d_st, d_pk = states, packets
         if not isinstance(d_pk, torch.Tensor) or not d_pk.is_cuda:

@@ -421,3 +421,23 @@ def test_multi_device_host_batches(oracle):
     assert np.array_equal(multi.highway_ragged(key, buf, off, None, 64, devices=[0, 0]), want)
     assert np.array_equal(multi.highway_ragged(key, buf, off[:-1], lens, 64, devices=[0, 0, 0]),
                           want)
+
+
+def test_read_only_host_inputs_zero_copy(oracle, tmp_path):
+    """Read-only host memory (a file opened as np.memmap mode "r",
+    np.frombuffer of bytes) is hashed without copies or warnings."""
+    import warnings
+
+    n, L = 4096, 96
+    data = synth.counter_bytes(12, n * L)
+    path = tmp_path / "msgs.bin"
+    data.tofile(path)
+    mm = np.memmap(path, dtype=np.uint8, mode="r", shape=(n, L))
+    key = synth.key256()
+    want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, data.reshape(n, L), 64, 4)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        assert np.array_equal(engine.highway_batch(key, mm), want)
+        ro = np.frombuffer(data.tobytes(), np.uint8)
+        off = np.arange(n + 1, dtype=np.uint64) * L
+        assert np.array_equal(engine.highway_ragged(key, ro, off), want)
