@@ -144,6 +144,19 @@ int lh_avalanche_counts(int alg, const uint64_t* key, const uint8_t* d_msgs,
  * device code is the Update every hashing kernel inlines. */
 int lh_highway_update_states(uint64_t* d_states, const uint64_t* d_packets,
                              uint64_t n, int inverse, void* stream);
+/* update_remainder (S/highway.py:182-199) on n caller states: tail i is
+ * d_tails[32i .. 32i + d_r[i]) (bytes beyond are ignored), d_r[i] in 1..31;
+ * a state whose d_r[i] is 0 or >= 32 is left unchanged (the reference
+ * raises ValueError for such tails, S/highway.py:185-186; the Python
+ * wrapper does, before launching). */
+int lh_highway_remainder_states(uint64_t* d_states, const uint8_t* d_tails,
+                                const uint32_t* d_r, uint64_t n, void* stream);
+/* finalize (S/highway.py:223-234) of n caller states: `rounds`
+ * PermuteAndUpdates, then width/64 lane sums per state into d_out
+ * (n x width/64 u64, lane 0 first).  States are not modified.  width 128
+ * is the derived width (lanes 0-1), as everywhere in this library. */
+int lh_highway_finalize_states(const uint64_t* d_states, uint64_t n, int width,
+                               int rounds, uint64_t* d_out, void* stream);
 /* Device self-test of the bijection on n synthetic cases: case i is words
  * 20i .. 20i+19 of the synthetic stream (seed, stream_id 0) -- 16 state
  * lanes, then 4 packet lanes.  ACCUMULATES (caller zeroes d_result[0..1]):

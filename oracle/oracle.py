@@ -48,6 +48,8 @@ def lib():
         l.lh_ref_zipper_bytes.argtypes = [u64, u64, vp, vp]
         l.lh_ref_hh_update.argtypes = [vp, vp]
         l.lh_ref_hh_update_inverse.argtypes = [vp, vp]
+        l.lh_ref_hh_update_remainder.argtypes = [vp, vp, ctypes.c_uint]
+        l.lh_ref_hh_finalize.argtypes = [vp, i32, vp]
         l.lh_ref_update_states.argtypes = [vp, vp, u64, i32]
         l.lh_ref_hh_init.argtypes = [vp, vp]
         l.lh_ref_hh_remainder_packet.argtypes = [vp, ctypes.c_uint, vp]

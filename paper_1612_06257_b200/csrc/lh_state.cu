@@ -1,8 +1,11 @@
-// lh_state.cu — the raw HighwayHash Update and its inverse on caller states,
-// and a device self-test of the bijection.
+// lh_state.cu — HighwayHash's state-level primitives on caller states, and
+// a device self-test of the Update bijection (SURVEY.md §8a rows a2, a4, a5,
+// a10 exposed one by one, as the reference module exposes them).
 //
-//   update         S/highway.py:130-150  (lh::Highway::update, the hot-path code)
-//   update_inverse S/highway.py:153-173  (lh::Highway::update_inverse)
+//   update           S/highway.py:130-150  (lh::Highway::update, the hot-path code)
+//   update_inverse   S/highway.py:153-173  (lh::Highway::update_inverse)
+//   update_remainder S/highway.py:182-199  (lh::Highway::remainder)
+//   finalize         S/highway.py:223-234  (lh::Highway::finalize_rounds + lane sums)
 //
 // The reference uses update_inverse only as a test oracle: the permutation
 // check of T/test_update.py:56-67 and the acceptance gate
@@ -54,6 +57,53 @@ __global__ void k_update_states(u64* __restrict__ states, const u64* __restrict_
     else
       h.update(p[0], p[1], p[2], p[3]);
     store_state(h, states + 16 * i);
+  }
+}
+
+// S/highway.py:182-199 on caller states: tail i is tails[32i .. 32i+r_i)
+// (bytes beyond r_i are ignored), r_i in 1..31; other r_i leave state i as is.
+__global__ void k_remainder_states(u64* __restrict__ states, const uint8_t* __restrict__ tails,
+                                   const u32* __restrict__ rs, u64 n, u32 one) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    const u32 r = rs[i];
+    if (r == 0 || r >= 32) continue;
+    Highway h;
+    h.one = one;
+    load_state(h, states + 16 * i);
+    u64 t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      u64 w = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) w |= (u64)tails[32 * i + 8 * k + b] << (8 * b);
+      t[k] = w;
+    }
+    h.remainder(t, r);
+    store_state(h, states + 16 * i);
+  }
+}
+
+// S/highway.py:223-234 on caller states: `rounds` PermuteAndUpdates, then
+// width/64 lane sums per state (lane 0 first).
+__global__ void k_finalize_states(const u64* __restrict__ states, u64 n, int width, int rounds,
+                                  u32 one, u64* __restrict__ out) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    Highway h;
+    h.one = one;
+    h.rounds = rounds;
+    h.width = width;
+    load_state(h, states + 16 * i);
+    h.finalize_rounds();
+    const int W = width / 64;
+    for (int k = 0; k < W; ++k) {
+      const u64 v0 = k == 0 ? h.v0[0] : k == 1 ? h.v0[1] : k == 2 ? h.v0[2] : h.v0[3];
+      const u64 v1 = k == 0 ? h.v1[0] : k == 1 ? h.v1[1] : k == 2 ? h.v1[2] : h.v1[3];
+      const u64 m0 = k == 0 ? h.m0[0] : k == 1 ? h.m0[1] : k == 2 ? h.m0[2] : h.m0[3];
+      const u64 m1 = k == 0 ? h.m1[0] : k == 1 ? h.m1[1] : k == 2 ? h.m1[2] : h.m1[3];
+      out[i * W + k] = v0 + v1 + m0 + m1;
+    }
   }
 }
 
@@ -122,6 +172,28 @@ int lh_highway_update_states(uint64_t* d_states, const uint64_t* d_packets, uint
     k_update_states<true><<<g, 256, 0, st>>>(d_states, d_packets, n, 1u);
   else
     k_update_states<false><<<g, 256, 0, st>>>(d_states, d_packets, n, 1u);
+  return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
+}
+
+int lh_highway_remainder_states(uint64_t* d_states, const uint8_t* d_tails,
+                                const uint32_t* d_r, uint64_t n, void* stream) {
+  if (n && (!d_states || !d_tails || !d_r)) return LH_EINVAL;
+  if ((uintptr_t)d_states % 8 || (uintptr_t)d_r % 4) return LH_EALIGN;
+  if (!n) return LH_OK;
+  k_remainder_states<<<grid_for(n, sm_count()), 256, 0, (cudaStream_t)stream>>>(
+      d_states, d_tails, d_r, n, 1u);
+  return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
+}
+
+int lh_highway_finalize_states(const uint64_t* d_states, uint64_t n, int width, int rounds,
+                               uint64_t* d_out, void* stream) {
+  if (width != 64 && width != 128 && width != 256) return LH_EINVAL;
+  if (rounds < 0) return LH_EINVAL;
+  if (n && (!d_states || !d_out)) return LH_EINVAL;
+  if ((uintptr_t)d_states % 8 || (uintptr_t)d_out % 8) return LH_EALIGN;
+  if (!n) return LH_OK;
+  k_finalize_states<<<grid_for(n, sm_count()), 256, 0, (cudaStream_t)stream>>>(
+      d_states, n, width, rounds, 1u, d_out);
   return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
 }
 

@@ -366,6 +366,49 @@ def update_states(states, packets, inverse: bool = False):
     return to_u64(d_st).reshape(n, 16) if host else d_st
 
 
+def remainder_states(states, tails, r):
+    """update_remainder (S/highway.py:182-199) of n raw states with tails
+    (n, 32) uint8 (bytes beyond r[i] ignored) and r (n,) in 1..31.  Host
+    arrays only; returns the new (n, 16) uint64 states."""
+    device = _require_cuda()
+    st = np.ascontiguousarray(states, dtype=np.uint64).reshape(-1, 16)
+    tl = np.ascontiguousarray(tails, dtype=np.uint8).reshape(-1, 32)
+    rr = np.ascontiguousarray(r, dtype=np.uint32).reshape(-1)
+    n = len(st)
+    if len(tl) != n or len(rr) != n:
+        raise ValueError("need (n,16) states, (n,32) tails and (n,) lengths")
+    if n and (rr.min() < 1 or rr.max() > 31):
+        raise ValueError("remainder length must be in 1..31")
+    if not n:
+        return st.copy()
+    d_st = torch.from_numpy(st.view(np.int64).copy()).to(device)
+    d_tl = _host_view(tl).to(device)
+    d_r = _host_view(rr.view(np.int32)).to(device)
+    rc = _lib.lib().lh_highway_remainder_states(d_st.data_ptr(), d_tl.data_ptr(), d_r.data_ptr(),
+                                                n, _stream_ptr(device))
+    _lib.check(rc, "lh_highway_remainder_states")
+    return to_u64(d_st).reshape(n, 16)
+
+
+def finalize_states(states, width: int = 64, rounds: int = 4) -> np.ndarray:
+    """finalize (S/highway.py:223-234) of n raw (n, 16) states: numpy
+    uint64 (n,) for width 64, else (n, width/64)."""
+    _check_width(width)
+    if rounds < 0:
+        raise ValueError("rounds must be >= 0")
+    device = _require_cuda()
+    st = np.ascontiguousarray(states, dtype=np.uint64).reshape(-1, 16)
+    n = len(st)
+    lanes = width // 64
+    out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=device)
+    if n:
+        d_st = _host_view(st.view(np.int64)).to(device)
+        rc = _lib.lib().lh_highway_finalize_states(d_st.data_ptr(), n, width, rounds,
+                                                   out.data_ptr(), _stream_ptr(device))
+        _lib.check(rc, "lh_highway_finalize_states")
+    return to_u64(out)
+
+
 def bijectivity(seed: int, n: int):
     """Device self-test: (failures, fold) over n synthetic (state, packet)
     cases, case i = words 20i..20i+19 of synth stream (seed, 0)."""

@@ -129,12 +129,10 @@ def _state_op(state: State, packet: Sequence[int], inverse: bool) -> State:
     from . import engine
     import numpy as np
 
-    if len(state) != 4 or any(len(x) != 4 for x in state) or len(packet) != 4:
-        raise ValueError("state is four 4-lane tuples and packet four lanes")
-    st = np.array([[x & _MASK64 for lanes in state for x in lanes]], dtype=np.uint64)
+    if len(packet) != 4:
+        raise ValueError("packet is four 64-bit lanes")
     pk = np.array([[x & _MASK64 for x in packet]], dtype=np.uint64)
-    out = [int(x) for x in engine.update_states(st, pk, inverse)[0]]
-    return tuple(tuple(out[i:i + 4]) for i in range(0, 16, 4))
+    return _unflat(engine.update_states(_flat(state), pk, inverse)[0])
 
 
 def update(state: State, packet: Sequence[int]) -> State:
@@ -145,6 +143,86 @@ def update(state: State, packet: Sequence[int]) -> State:
 def update_inverse(state: State, packet: Sequence[int]) -> State:
     """Exact inverse of :func:`update` (S/highway.py:153-173) on the GPU."""
     return _state_op(state, packet, True)
+
+
+def _flat(state: State):
+    import numpy as np
+
+    if len(state) != 4 or any(len(x) != 4 for x in state):
+        raise ValueError("state is four 4-lane tuples")
+    return np.array([[x & _MASK64 for lanes in state for x in lanes]], dtype=np.uint64)
+
+
+def _unflat(row) -> State:
+    out = [int(x) for x in row]
+    return tuple(tuple(out[i:i + 4]) for i in range(0, 16, 4))
+
+
+def update_remainder(state: State, tail: bytes) -> State:
+    """Absorb the final 1..31 bytes plus the length injection
+    (S/highway.py:182-199), on the GPU engine (lh::Highway::remainder)."""
+    from . import engine
+    import numpy as np
+
+    tail = bytes(tail)
+    if not 1 <= len(tail) <= 31:
+        raise ValueError("remainder length must be in 1..31")
+    t = np.zeros((1, 32), np.uint8)
+    t[0, :len(tail)] = np.frombuffer(tail, np.uint8)
+    return _unflat(engine.remainder_states(_flat(state), t, [len(tail)])[0])
+
+
+def finalize(state: State, width: int = 64, rounds: int = 4):
+    """`rounds` PermuteAndUpdates and the lane sums (S/highway.py:223-234),
+    on the GPU engine: an int for width 64, a tuple of width/64 lanes
+    otherwise (128 is this library's derived width)."""
+    from . import engine
+
+    _check_width(width)
+    out = engine.finalize_states(_flat(state), width, rounds)
+    return int(out[0]) if width == 64 else tuple(int(x) for x in out[0])
+
+
+# Byte-layout helpers of the reference module.  They only rearrange bytes
+# and never feed the engine, which builds packets in registers
+# (lh_device.cuh); they exist so code written against lanehash.highway runs.
+
+def packet_lanes(packet: bytes) -> Tuple[int, int, int, int]:
+    """32 bytes as four little-endian 64-bit lanes (S/highway.py:115-119)."""
+    if len(packet) != 32:
+        raise ValueError("packet must be exactly 32 bytes")
+    return struct.unpack("<4Q", bytes(packet))
+
+
+def remainder_packet(tail: bytes) -> bytes:
+    """The 32-byte packet of a 1..31 byte remainder (S/highway.py:206-220):
+    whole 4-byte groups first, the 0..3 leftover bytes at bytes 28..31."""
+    r = len(tail)
+    if not 1 <= r <= 31:
+        raise ValueError("remainder length must be in 1..31")
+    whole = r & ~3
+    packet = bytearray(32)
+    packet[:whole] = bytes(tail[:whole])
+    packet[28:28 + r - whole] = bytes(tail[whole:])
+    return bytes(packet)
+
+
+def permute_lanes(v: Sequence[int]) -> Tuple[int, int, int, int]:
+    """PermuteAndUpdate's packet (S/highway.py:176-179)."""
+    a, b, c, d = v
+    return (_rot32(c), _rot32(d), _rot32(a), _rot32(b))
+
+
+def zipper_merge(half: bytes) -> bytes:
+    """ZIPPER_OFFSETS applied to one 16-byte lane pair (S/highway.py:73-77)."""
+    if len(half) != 16:
+        raise ValueError("zipper_merge operates on exactly 16 bytes")
+    return bytes(half[off] for off in ZIPPER_OFFSETS)
+
+
+def mul32(a: int, b: int) -> int:
+    """Low 32 bits of a times low 32 bits of b (S/highway.py:80-82)."""
+    return ((a & 0xFFFFFFFF) * (b & 0xFFFFFFFF)) & _MASK64
 
 
 class StreamingHasher:
