@@ -157,6 +157,10 @@ int lh_highway_remainder_states(uint64_t* d_states, const uint8_t* d_tails,
  * is the derived width (lanes 0-1), as everywhere in this library. */
 int lh_highway_finalize_states(const uint64_t* d_states, uint64_t n, int width,
                                int rounds, uint64_t* d_out, void* stream);
+/* sip_round (S/sip.py:73-86) applied `rounds` times to n caller states
+ * (n x 4 u64: v0, v1, v2, v3), in place -- the round every SipHash /
+ * SipTreeHash kernel inlines. */
+int lh_sip_round_states(uint64_t* d_states, uint64_t n, int rounds, void* stream);
 /* Device self-test of the bijection on n synthetic cases: case i is words
  * 20i .. 20i+19 of the synthetic stream (seed, stream_id 0) -- 16 state
  * lanes, then 4 packet lanes.  ACCUMULATES (caller zeroes d_result[0..1]):

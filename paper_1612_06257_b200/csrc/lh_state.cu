@@ -6,6 +6,7 @@
 //   update_inverse   S/highway.py:153-173  (lh::Highway::update_inverse)
 //   update_remainder S/highway.py:182-199  (lh::Highway::remainder)
 //   finalize         S/highway.py:223-234  (lh::Highway::finalize_rounds + lane sums)
+//   sip_round        S/sip.py:73-86        (lh::sip_round, the SipHash kernels' round)
 //
 // The reference uses update_inverse only as a test oracle: the permutation
 // check of T/test_update.py:56-67 and the acceptance gate
@@ -107,6 +108,20 @@ __global__ void k_finalize_states(const u64* __restrict__ states, u64 n, int wid
   }
 }
 
+// S/sip.py:73-86: `rounds` SipRounds on n caller states (4 lanes each).
+__global__ void k_sip_round_states(u64* __restrict__ states, u64 n, int rounds, SipMul k) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    u64 v0 = states[4 * i], v1 = states[4 * i + 1], v2 = states[4 * i + 2],
+        v3 = states[4 * i + 3];
+    for (int r = 0; r < rounds; ++r) sip_round(v0, v1, v2, v3, k);
+    states[4 * i] = v0;
+    states[4 * i + 1] = v1;
+    states[4 * i + 2] = v2;
+    states[4 * i + 3] = v3;
+  }
+}
+
 // Case i = words 20i .. 20i+19 of the synthetic stream: 16 state lanes, then
 // 4 packet lanes.  result[0] += failures, result[1] ^= fold of update(s).
 __global__ void k_bijectivity(u64 key, u64 n, u32 one, unsigned long long* result) {
@@ -194,6 +209,16 @@ int lh_highway_finalize_states(const uint64_t* d_states, uint64_t n, int width, 
   if (!n) return LH_OK;
   k_finalize_states<<<grid_for(n, sm_count()), 256, 0, (cudaStream_t)stream>>>(
       d_states, n, width, rounds, 1u, d_out);
+  return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
+}
+
+int lh_sip_round_states(uint64_t* d_states, uint64_t n, int rounds, void* stream) {
+  if (rounds < 0 || (n && !d_states)) return LH_EINVAL;
+  if ((uintptr_t)d_states % 8) return LH_EALIGN;
+  if (!n || !rounds) return LH_OK;
+  const SipMul k = {1u, 1u << 13, 1u << 17, 1u << 21};
+  k_sip_round_states<<<grid_for(n, sm_count()), 256, 0, (cudaStream_t)stream>>>(d_states, n,
+                                                                                rounds, k);
   return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;
 }
 

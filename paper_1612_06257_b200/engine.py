@@ -409,6 +409,21 @@ def finalize_states(states, width: int = 64, rounds: int = 4) -> np.ndarray:
     return to_u64(out)
 
 
+def sip_round_states(states, rounds: int = 1) -> np.ndarray:
+    """`rounds` SipRounds (S/sip.py:73-86) of n (n, 4) uint64 host states;
+    returns the new states."""
+    if rounds < 0:
+        raise ValueError("rounds must be >= 0")
+    device = _require_cuda()
+    st = np.ascontiguousarray(states, dtype=np.uint64).reshape(-1, 4)
+    if not len(st):
+        return st.copy()
+    d_st = torch.from_numpy(st.view(np.int64).copy()).to(device)
+    rc = _lib.lib().lh_sip_round_states(d_st.data_ptr(), len(st), rounds, _stream_ptr(device))
+    _lib.check(rc, "lh_sip_round_states")
+    return to_u64(d_st).reshape(-1, 4)
+
+
 def bijectivity(seed: int, n: int):
     """Device self-test: (failures, fold) over n synthetic (state, packet)
     cases, case i = words 20i..20i+19 of synth stream (seed, 0)."""

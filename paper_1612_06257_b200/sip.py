@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import struct
 from dataclasses import dataclass
+from typing import Tuple
 
 _MASK64 = 0xFFFFFFFFFFFFFFFF
 
@@ -74,6 +75,30 @@ class SipParams:
 
 SIPHASH_24 = SipParams(2, 4)
 SIPHASH_13 = SipParams(1, 3)
+
+
+def sip_round(state: Tuple[int, int, int, int]) -> Tuple[int, int, int, int]:
+    """One SipRound (S/sip.py:73-86) on the GPU engine (lh::sip_round)."""
+    from . import engine
+    import numpy as np
+
+    if len(state) != 4:
+        raise ValueError("state is four 64-bit words")
+    st = np.array([[x & _MASK64 for x in state]], dtype=np.uint64)
+    return tuple(int(x) for x in engine.sip_round_states(st, 1)[0])
+
+
+def deinterleave(message: bytes) -> Tuple[bytes, bytes, bytes, bytes]:
+    """SipTreeHash's lane split (S/sip.py:111-121): zero-pad to a multiple
+    of 32 bytes (empty stays empty); lane j gets words 4i + j.  A byte-layout
+    helper: the engine reads lanes straight from the message (lh::SipTree)."""
+    message = bytes(message)
+    if message and len(message) % 32:
+        message += bytes(32 - len(message) % 32)
+    lanes = [bytearray(), bytearray(), bytearray(), bytearray()]
+    for i in range(0, len(message), 8):
+        lanes[(i // 8) % 4] += message[i:i + 8]
+    return tuple(bytes(x) for x in lanes)
 
 
 def siphash(key, message: bytes, params: SipParams = SIPHASH_24) -> int:
