@@ -33,20 +33,25 @@ class SizeRow:
     ns_per_byte: float
     bytes_per_ns: float
     msgs_per_s: float
+    digest_fold: int  # XOR of every digest word of the last launch
 
 
 def sweep(algo_name: str, sizes: Sequence[int], batch_bytes: int = 1 << 30,
-          steps: int = 10, warmup: int = 3, seed: int = 0) -> List[SizeRow]:
+          steps: int = 10, warmup: int = 3, seed: int = 0, runs: int = 1) -> List[SizeRow]:
+    """One row per size.  `runs` repeats the timed block per size; the row
+    reports the median over runs of the per-run median launch time (the
+    reference's estimator shape, S/bench.py:161-182)."""
     import torch
 
     from . import engine, synth
     from .catalog import get_algorithm
 
+    if steps < 1 or runs < 1:
+        raise ValueError("steps and runs must be >= 1")
     algo = get_algorithm(algo_name)
     dev = torch.device("cuda", torch.cuda.current_device())
     key = synth.key256() if algo.key_size == 32 else synth.key128()
     rows = []
-    checksum = 0
     for L in sizes:
         n = max(1 << 16, min(1 << 26, batch_bytes // max(L, 1)))
         buf = torch.empty(max(1, n * L), dtype=torch.uint8, device=dev)
@@ -64,20 +69,21 @@ def sweep(algo_name: str, sizes: Sequence[int], batch_bytes: int = 1 << 30,
         for _ in range(warmup):
             step()
         st = torch.cuda.current_stream(dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-        ev[0].record(st)
-        for i in range(steps):
-            step()
-            ev[i + 1].record(st)
-        torch.cuda.synchronize()
-        ms = float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]))
-        checksum ^= int(np.bitwise_xor.reduce(engine.to_u64(out).reshape(-1)))
+        run_ms = []
+        for _ in range(runs):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+            ev[0].record(st)
+            for i in range(steps):
+                step()
+                ev[i + 1].record(st)
+            torch.cuda.synchronize()
+            run_ms.append(float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(steps)])))
+        ms = float(np.median(run_ms))
+        fold = int(np.bitwise_xor.reduce(engine.to_u64(out).reshape(-1)))
         nbytes = n * L
         rows.append(SizeRow(algo_name, L, n, ms, ms * 1e6 / nbytes if nbytes else float("nan"),
-                            nbytes / (ms * 1e6) if ms else float("inf"), n / ms * 1e3))
+                            nbytes / (ms * 1e6) if ms else float("inf"), n / ms * 1e3, fold))
         del buf, out
-    if checksum == 0 and rows:  # pragma: no cover - digests consumed
-        pass
     return rows
 
 

@@ -79,3 +79,112 @@ def test_gpubench_presets():
     assert gpubench.PRESETS["table1"] == (8, 31, 32, 63, 64, 1024)
     rows = gpubench.sweep("highway64", [1, 33], batch_bytes=1 << 20, steps=2)
     assert [r.size for r in rows] == [1, 33] and all(r.msgs_per_s > 0 for r in rows)
+
+
+# T/test_vectors_cli.py, one test per test (first8bytes is a reference-only
+# control hash, out of scope: DESIGN.md §0).
+def run_cli(capsys, *argv):
+    code = cli.main(list(argv))
+    cap = capsys.readouterr()
+    return code, cap.out, cap.err
+
+
+def test_generate_covers_all_algorithms_and_lengths():
+    from paper_1612_06257_b200.catalog import VECTOR_ALGORITHMS
+
+    records = vectors.generate()
+    assert len(records) == len(VECTOR_ALGORITHMS) * len(vectors.DEFAULT_LENGTHS)
+    lengths = {len(r.message_hex) // 2 for r in records if r.algo == "highway64"}
+    assert {0, 31, 32, 33, 64, 256, 1023, 1024} <= lengths
+    assert {r.algo for r in records} == set(VECTOR_ALGORITHMS)
+
+
+def test_vector_round_trip_and_verify():
+    records = vectors.generate(lengths=[0, 5, 32, 33])
+    buf = io.StringIO()
+    vectors.write(records, buf)
+    buf.seek(0)
+    parsed = vectors.read(buf)
+    assert parsed == records and vectors.verify(parsed) == []
+
+
+def test_read_skips_comments_and_blank_lines():
+    line = vectors.generate(algos=["siphash24"], lengths=[1])[0].to_line()
+    assert len(vectors.read(io.StringIO(f"# header\n\n{line}\n"))) == 1
+
+
+def test_cli_vectors_stdout_format(capsys):
+    from paper_1612_06257_b200.catalog import VECTOR_ALGORITHMS
+
+    code, out, _ = run_cli(capsys, "vectors")
+    lines = out.strip().splitlines()
+    assert code == 0 and len(lines) == len(VECTOR_ALGORITHMS) * len(vectors.DEFAULT_LENGTHS)
+    first = lines[0].split(",")
+    assert len(first) == 4 and first[0] == "highway64"
+
+
+def test_cli_hash_published_sip_vector(tmp_path, capsys):
+    empty = tmp_path / "empty"
+    empty.write_bytes(b"")
+    code, out, _ = run_cli(capsys, "hash", "--algo", "siphash24", "--key",
+                           "000102030405060708090a0b0c0d0e0f", str(empty))
+    assert code == 0 and out.split()[0] == "310e0edd47db6f72"
+
+
+def test_cli_hash_stdin_matches_file(tmp_path, capsys, monkeypatch):
+    import sys
+
+    data = bytes(range(200))
+    path = tmp_path / "data"
+    path.write_bytes(data)
+    code, out_file, _ = run_cli(capsys, "hash", str(path))
+    monkeypatch.setattr(sys, "stdin", type("S", (), {"buffer": io.BytesIO(data)})())
+    code2, out_stdin, _ = run_cli(capsys, "hash")
+    assert code == code2 == 0
+    assert out_file.split()[0] == out_stdin.split()[0] and out_stdin.split()[1] == "-"
+
+
+def test_cli_hash_width_256(tmp_path, capsys):
+    path = tmp_path / "data"
+    path.write_bytes(b"abc")
+    code, out, _ = run_cli(capsys, "hash", "--algo", "highway", "--width", "256", str(path))
+    assert code == 0 and len(out.split()[0]) == 64
+
+
+def test_cli_hash_unreadable_input_exits_1(tmp_path, capsys):
+    code, _, err = run_cli(capsys, "hash", str(tmp_path / "missing"))
+    assert code == 1 and "cannot read" in err
+
+
+def test_cli_avalanche_real_hash_passes(capsys):
+    code, out, _ = run_cli(capsys, "avalanche", "--algo", "siphash24", "--sizes", "4",
+                           "--iters", "100000", "--samples", "3")
+    rows = [l for l in out.splitlines() if not l.startswith("#")]
+    assert code == 0 and len(rows) == 1
+    algo, size, bias, threshold, state = rows[0].split(",")
+    assert (algo, size, state) == ("siphash24", "4", "pass") and float(bias) < float(threshold)
+
+
+def test_cli_bench_rows(capsys):
+    code, out, _ = run_cli(capsys, "bench", "--algo", "siphash13", "--sizes", "8,64", "--reps",
+                           "9", "--runs", "1", "--batch-mib", "64")
+    machine_rows = [l for l in out.splitlines() if l.startswith("siphash13,")]
+    assert code == 0 and len(machine_rows) == 2 and machine_rows[0].split(",")[1] == "8"
+
+
+def test_module_entry_point_smoke(tmp_path):
+    """T/test_vectors_cli.py:205-214, with `python -m` standing in for the
+    installed console script."""
+    import os
+    import subprocess
+    import sys
+
+    path = tmp_path / "data"
+    path.write_bytes(b"hello")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    proc = subprocess.run([sys.executable, "-m", "paper_1612_06257_b200", "hash", str(path)],
+                          capture_output=True, text=True, cwd=root)
+    assert proc.returncode == 0
+    digest = proc.stdout.split()[0]
+    assert len(digest) == 16
+    int(digest, 16)

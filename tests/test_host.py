@@ -202,3 +202,17 @@ def test_cli_rejects_bad_arguments_before_hashing():
     with pytest.raises(ValueError):
         vectors.VectorRecord.from_line("a,b,c")
     assert vectors.ramp(3) == b"\x00\x01\x02"
+    for argv in (["avalanche", "--sizes", "40", "--iters", "10"],
+                 ["avalanche", "--sizes", "abc"], ["bench", "--reps", "0", "--sizes", "8"],
+                 ["bench", "--runs", "0", "--sizes", "8"]):
+        with pytest.raises(SystemExit):
+            cli.main(argv)
+
+
+def test_cli_size_range_parsing():
+    """T/test_vectors_cli.py:199-202."""
+    from paper_1612_06257_b200 import cli
+
+    parser = cli.build_parser()
+    assert cli._parse_sizes(parser, "4..6") == [4, 5, 6]
+    assert cli._parse_sizes(parser, "1,8..10,32") == [1, 8, 9, 10, 32]
