@@ -82,3 +82,32 @@ def test_finalization_variant(oracle):
         f = finalization_variant(r)
         for msg in (b"", b"abc", bytes(range(33))):
             assert f(key, msg) == oracle.highway(lanes, msg, r)[0]
+
+
+# T/test_quality.py, the device-side tests one by one.
+def test_avalanche_seed_reproducibility():
+    h = quality.HashUnderTest.from_name("siphash13")
+    a = quality.avalanche_bias(h, size=4, iterations=200, seed=7)
+    b = quality.avalanche_bias(h, size=4, iterations=200, seed=7)
+    c = quality.avalanche_bias(h, size=4, iterations=200, seed=8)
+    assert np.array_equal(a.counts, b.counts)
+    assert not np.array_equal(a.counts, c.counts)
+
+
+def test_run_avalanche_passes_real_hash_above_noise():
+    report = quality.run_avalanche(quality.HashUnderTest.from_name("siphash24"), sizes=[4],
+                                   iterations=50_000, samples=3)
+    assert report.passed
+    assert report.verdicts[0].noise_floor == pytest.approx(0.5 / 50_000 ** 0.5)
+
+
+def test_zero_input_distinctness_real_hash():
+    good = quality.zero_input_distinctness(quality.HashUnderTest.from_name("highway64"),
+                                           max_size=256)
+    assert good.distinct and good.imbalance() < 0.25
+
+
+def test_finalization_experiment_shapes():
+    res = quality.finalization_bias_experiment(4, inputs=500, seed=1)
+    assert (res.rounds, res.inputs, res.exhaustive) == (4, 500, False)
+    assert 0.0 <= res.max_bias <= 0.5 and 0.0 <= res.mean_bias <= res.max_bias
