@@ -82,6 +82,7 @@ class ClockSampler:
 
     def __init__(self, index: int, period: float = 0.05, enabled: bool = True):
         self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.power_mw, self.power_limit_mw = [], None
         self.period, self._stop = period, threading.Event()
         self.ok = False
         if not enabled:
@@ -93,6 +94,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = self._handle(pynvml, index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.power_limit_mw = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h)
+            except Exception:
+                pass
             self.ok = True
         except Exception:
             pass
@@ -110,10 +115,25 @@ class ClockSampler:
         except Exception:
             return pynvml.nvmlDeviceGetHandleByIndex(index)
 
+    def _power_mw(self):
+        """Instantaneous board power (NVML_FI_DEV_POWER_INSTANT); the plain
+        power reading is a ~1 s average that lags a 100 ms timed region."""
+        nv = self.nv
+        try:
+            fv = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+            if fv.nvmlReturn == 0:
+                v = fv.value
+                return int({0: v.dVal, 1: v.uiVal, 2: v.ulVal, 3: v.ullVal, 4: v.sllVal,
+                            5: v.siVal}.get(fv.valueType, v.uiVal))
+        except Exception:
+            pass
+        return nv.nvmlDeviceGetPowerUsage(self.h)
+
     def _sample(self):
         try:
             self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
             self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            self.power_mw.append(self._power_mw())
         except Exception:
             pass
 
@@ -139,8 +159,14 @@ class ClockSampler:
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
         reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
-        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples)}
+        out = {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+               "reasons": reasons, "samples": len(self.samples)}
+        if self.power_mw:  # board power while timing, against the enforced limit
+            out["power_w"] = round(float(np.median(self.power_mw)) / 1e3, 1)
+            out["power_w_max"] = round(max(self.power_mw) / 1e3, 1)
+        if self.power_limit_mw:
+            out["power_limit_w"] = round(self.power_limit_mw / 1e3, 1)
+        return out
 
 
 def _dist_env():
