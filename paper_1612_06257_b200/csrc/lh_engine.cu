@@ -371,10 +371,13 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
                              (int32_t)(pf_tile * ROWS + b * kBoxRowsTma));
         if (++pf_c == nchunks) { pf_c = 0; pf_tile += gridDim.x; }
       }
-      u32 it = 0;
+      // Every message tile restarts at stage 0 (the consumers unroll over
+      // stages per tile); `used` bit s = parity of the uses of stage s.
+      u32 used = 0;
       for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (u32 c = 0; c < nchunks; ++c, ++it) {
-          const u32 s = it % STAGES, ph = (it / STAGES) & 1;
+        for (u32 c = 0; c < nchunks; ++c) {
+          const u32 s = c % STAGES, ph = (used >> s) & 1;
+          used ^= 1u << s;
           mbar_wait(&empty_bar[s], ph ^ 1);
           mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
 #pragma unroll
@@ -408,22 +411,28 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   const int W = nout(proto);
   const u64 nfull = len >> 5;
   const u32 r = (u32)(len & 31);  // 0 or 16
-  u32 it = 0;
+  // Each message tile starts at stage 0 and the chunk loop is unrolled over
+  // the STAGES ring slots, so in each copy the stage -- its barriers and LDS
+  // offsets -- is a compile-time constant; `used` bit s is the parity of
+  // stage s's uses (a tile whose chunk count is not a multiple of STAGES
+  // leaves the last slots of its final round unused).  Per chunk: one
+  // wait, one compare, the arrive and a bit flip; the message epilogue is a
+  // single copy outside the unrolled body (I-cache: the Sip bodies are big).
+  const u32 nfull4 = (u32)(nfull >> 2);  // chunks that hold 4 whole packets
+  u32 bars;  // shared address of full_bar[0]; empty_bar[s] = bars + 8 * (STAGES + s)
+  asm volatile("mov.b32 %0, %1;" : "=r"(bars) : "r"(smem_u32(full_bar)));
+  u32 used = 0;
   for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     H h = proto;
     u64 tl[4] = {0, 0, 0, 0};
-    for (u32 c = 0; c < nchunks; ++c, ++it) {
-      const u32 s = it % STAGES, ph = (it / STAGES) & 1;
-      mbar_wait(&full_bar[s], ph);
-      const u32 so = s * kStageBytes;
-      const u64 left = nfull - (u64)c * 4;
-      const u32 kvalid = left >= 4 ? 4u : (u32)left;
-      if (kvalid == 4) {
-        // One copy of the 4-packet body per stage, so `so` is a compile-time
-        // LDS offset (no per-chunk address arithmetic on the ALU pipe).
+    for (u32 cb = 0; cb < nchunks; cb += STAGES) {
 #pragma unroll
-        for (u32 ss = 0; ss < (u32)STAGES; ++ss) {
-          if (s == ss) {
+      for (u32 ss = 0; ss < (u32)STAGES; ++ss) {
+        const u32 c = cb + ss;
+        if (c < nchunks) {
+          mbar_wait_addr(bars + 8 * ss, (used >> ss) & 1);
+          used ^= 1u << ss;
+          if (c < nfull4) {
 #pragma unroll
             for (u32 k = 0; k < 4; ++k) {
               const uint4 a = lds128(ua[2 * k] + ss * kStageBytes);
@@ -431,24 +440,27 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
               const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
               h.absorb32(p);
             }
+          } else {
+            // Last chunk of a message whose length is not a multiple of
+            // 128: 0..3 whole packets, then the 16-byte tail if r != 0.
+            const u32 kvalid = (u32)(nfull - 4ull * c);
+            const u32 rowa = row0 + ss * kStageBytes;
+            for (u32 k = 0; k < kvalid; ++k) {
+              const uint4 a = lds128(rowa + (((2 * k) ^ sw) << 4));
+              const uint4 b = lds128(rowa + (((2 * k + 1) ^ sw) << 4));
+              const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
+              h.absorb32(p);
+            }
+            if (r) {
+              const uint4 a = lds128(rowa + (((2 * kvalid) ^ sw) << 4));
+              tl[0] = pack(a.x, a.y);
+              tl[1] = pack(a.z, a.w);
+            }
           }
-        }
-      } else {
-        const u32 rowa = row0 + so;
-        for (u32 k = 0; k < kvalid; ++k) {
-          const uint4 a = lds128(rowa + (((2 * k) ^ sw) << 4));
-          const uint4 b = lds128(rowa + (((2 * k + 1) ^ sw) << 4));
-          const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
-          h.absorb32(p);
-        }
-        if (r) {
-          const uint4 a = lds128(rowa + (((2 * kvalid) ^ sw) << 4));
-          tl[0] = pack(a.x, a.y);
-          tl[1] = pack(a.z, a.w);
+          __syncwarp();
+          if (lane == 0) mbar_arrive_addr(bars + 8 * (STAGES + ss));
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
     const u64 row_idx = tile * ROWS + t;
     if (row_idx < n) h.finish(tl, r, len, out + row_idx * W);
