@@ -177,10 +177,12 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
 // --------------------------------------------------------------------------
 // Ragged short-message kernel (cfg3: 2^26 keys of 8..64 bytes, finalization
 // dominated).  Each warp takes 32 consecutive messages.  Fast path (every
-// message <= 64 B and the warp's byte span <= kSpanCap): the warp copies the
-// span into shared memory with coalesced 16-byte loads, each thread builds
-// its message's 16 little-endian 32-bit words with funnel shifts (bytes past
-// the end zeroed), and runs exactly two non-divergent Update slots:
+// message <= 64 B and inside the kSpanCap-byte window that starts at lane
+// 0's message): the warp copies the window into shared memory with
+// coalesced 16-byte loads, each thread builds its message's 16 little-endian
+// 32-bit words with funnel shifts (bytes past the end are left as they are
+// and never reach a packet unmasked), and runs exactly two non-divergent
+// Update slots:
 //   slot s (s = 0, 1): full block s if s < nfull, else the remainder
 //   packet of the tail if s == nfull and r > 0, else nothing;
 // the remainder's length injection is applied unconditionally with r_eff =
@@ -189,21 +191,6 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
 // offsets) takes the generic per-thread path (hash_direct).
 // --------------------------------------------------------------------------
 constexpr u32 kSpanCap = 2048;  // bytes of a warp's span staged in smem
-
-// Remainder packet (S/highway.py:206-220) from the tail's 8 words (zero past
-// r): word q = r/4 (the 0..3 leftover bytes, LE) moves to packet word 7.
-__device__ __forceinline__ void rem_packet_words(const u32 (&T)[8], u32 r, u64 (&p)[4]) {
-  const u32 q = r >> 2;
-  u32 P[8];
-  u32 lft = T[0];
-#pragma unroll
-  for (u32 j = 1; j < 8; ++j) lft = (q == j) ? T[j] : lft;
-#pragma unroll
-  for (u32 j = 0; j < 7; ++j) P[j] = (q == j) ? 0u : T[j];
-  P[7] = lft;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) p[k] = pack(P[2 * k], P[2 * k + 1]);
-}
 
 // Length injection of UpdateRemainder (S/highway.py:188-197); r = 0 is a no-op.
 __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
@@ -240,15 +227,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
         len = fixed_len;
       }
     }
-    u64 lo = valid ? start : ~0ull, hi = valid ? start + len : 0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const u64 a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
-      lo = a < lo ? a : lo;
-      hi = b > hi ? b : hi;
-    }
-    const u32 maxlen = __reduce_max_sync(0xffffffffu, (u32)(len > 0xffffffffull ? 0xffffffffu : len));
-    if (maxlen <= 64 && hi - lo <= kSpanCap) {
+    // Fast-path test with 32-bit warp reductions: every message lies in the
+    // window [s0, s0 + kSpanCap) that starts at lane 0's message (lane 0 is
+    // always valid) and is at most 64 bytes.  Packed batches always pass.
+    const u64 s0 = __shfl_sync(0xffffffffu, start, 0);
+    const bool fits = !valid || (len <= 64 && start >= s0 && start + len - s0 <= kSpanCap);
+    if (__all_sync(0xffffffffu, fits)) {
+      const u32 span = __reduce_max_sync(0xffffffffu, valid ? (u32)(start + len - s0) : 0u);
+      const u64 lo = s0, hi = s0 + span;
       // Align on the absolute address: d_buf itself need not be 16-B aligned.
       const u64 base = (u64)(uintptr_t)buf;
       const u64 lo_al = ((base + lo) & ~15ull) - base, hi_al = ((base + hi + 15) & ~15ull) - base;
@@ -259,15 +245,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       if (valid) {
         const u32 o = (u32)(start - lo_al), a = o >> 2, sh = (o & 3) * 8;
         const u32 L = (u32)len;
+        // The message's 16 LE words; bytes past L belong to other messages
+        // and are never used unmasked (see the packet selection below).
         u32 Wd[16];
         u32 cur = S[a];
 #pragma unroll
         for (u32 k = 0; k < 16; ++k) {
           const u32 nxt = S[a + k + 1];
-          u32 w = __funnelshift_r(cur, nxt, sh);
-          const int keep = (int)L - 4 * (int)k;  // bytes of word k inside the message
-          w &= keep >= 4 ? 0xffffffffu : (keep <= 0 ? 0u : ((1u << (8 * keep)) - 1u));
-          Wd[k] = w;
+          Wd[k] = __funnelshift_r(cur, nxt, sh);
           cur = nxt;
         }
         const u32 nfull = L >> 5, r = L & 31;
@@ -277,17 +262,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
           const bool full = s < nfull;
           const bool rem = (s == nfull) && r;
           if (full || rem) {
-            u32 T[8];
+            // Full block: the 8 words as they are.  Remainder packet
+            // (S/highway.py:206-220): whole words j < q = r/4 in place,
+            // zeros, and the r%4 leftover bytes of word q in word 7.
+            const u32 q = full ? 8u : (r >> 2);
+            const u32 nleft = full ? 4u : (r & 3u);
+            u32 P[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) T[j] = Wd[8 * s + j];
-            u64 p[4];
-            rem_packet_words(T, rem ? r : 0u, p);
-            if (full) {
+            for (u32 j = 0; j < 7; ++j) P[j] = j < q ? Wd[8 * s + j] : 0u;
+            u32 lft = Wd[8 * s + 7];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) p[k] = pack(T[2 * k], T[2 * k + 1]);
-            }
+            for (u32 j = 0; j < 7; ++j) lft = (q == j) ? Wd[8 * s + j] : lft;
+            P[7] = lft & (nleft >= 4 ? 0xffffffffu : ((1u << (8 * nleft)) - 1u));
             rem_tweak(h, rem ? r : 0u);
-            h.update(p[0], p[1], p[2], p[3]);
+            h.update(pack(P[0], P[1]), pack(P[2], P[3]), pack(P[4], P[5]), pack(P[6], P[7]));
           }
         }
         h.finalize_rounds();
