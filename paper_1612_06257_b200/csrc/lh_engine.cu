@@ -179,15 +179,14 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
 // dominated).  Each warp takes 32 consecutive messages.  Fast path (every
 // message <= 64 B and inside the kSpanCap-byte window that starts at lane
 // 0's message): the warp copies the window into shared memory with
-// coalesced 16-byte loads, each thread builds its message's 16 little-endian
-// 32-bit words with funnel shifts (bytes past the end are left as they are
-// and never reach a packet unmasked), and runs exactly two non-divergent
-// Update slots:
-//   slot s (s = 0, 1): full block s if s < nfull, else the remainder
-//   packet of the tail if s == nfull and r > 0, else nothing;
-// the remainder's length injection is applied unconditionally with r_eff =
-// r or 0 (adding 0 / rotating by 0 is the identity), so lanes with different
-// lengths never split the Update.  Any other warp (long messages, scattered
+// coalesced 16-byte loads, each thread reads its message's little-endian
+// 32-bit words from it with funnel shifts (bytes past the end are never
+// used unmasked), and runs two non-divergent Update slots:
+//   slot 0: block 0 if the message has one;
+//   slot 1: block 1 (64-byte messages) or the remainder packet (r > 0),
+// so lanes of different lengths share both Updates, and the remainder's
+// length injection, done in slot 1 with r_eff = r or 0 (adding 0 / rotating
+// by 0 is the identity), is the only one.  Any other warp (long messages, scattered
 // offsets) takes the generic per-thread path (hash_direct).
 // --------------------------------------------------------------------------
 constexpr u32 kSpanCap = 2048;  // bytes of a warp's span staged in smem
@@ -245,38 +244,33 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       if (valid) {
         const u32 o = (u32)(start - lo_al), a = o >> 2, sh = (o & 3) * 8;
         const u32 L = (u32)len;
-        // The message's 16 LE words; bytes past L belong to other messages
-        // and are never used unmasked (see the packet selection below).
-        u32 Wd[16];
-        u32 cur = S[a];
-#pragma unroll
-        for (u32 k = 0; k < 16; ++k) {
-          const u32 nxt = S[a + k + 1];
-          Wd[k] = __funnelshift_r(cur, nxt, sh);
-          cur = nxt;
-        }
         const u32 nfull = L >> 5, r = L & 31;
+        // Word k of the message (LE; bytes past L belong to other messages).
+        auto word = [&](u32 k) { return __funnelshift_r(S[a + k], S[a + k + 1], sh); };
         Highway h = proto;
+        // Slot 0: block 0 if the message has one (32..64 bytes); no tweak.
+        if (nfull) {
+          u32 P[8];
 #pragma unroll
-        for (u32 s = 0; s < 2; ++s) {
-          const bool full = s < nfull;
-          const bool rem = (s == nfull) && r;
-          if (full || rem) {
-            // Full block: the 8 words as they are.  Remainder packet
-            // (S/highway.py:206-220): whole words j < q = r/4 in place,
-            // zeros, and the r%4 leftover bytes of word q in word 7.
-            const u32 q = full ? 8u : (r >> 2);
-            const u32 nleft = full ? 4u : (r & 3u);
-            u32 P[8];
+          for (u32 j = 0; j < 8; ++j) P[j] = word(j);
+          h.update(pack(P[0], P[1]), pack(P[2], P[3]), pack(P[4], P[5]), pack(P[6], P[7]));
+        }
+        // Slot 1: block 1 (64 bytes) or the remainder packet (r > 0) of the
+        // words from b = 8 * [nfull >= 1] on (S/highway.py:206-220): whole
+        // words j < q = r/4 in place, zeros, the r%4 leftover bytes of word q
+        // in word 7; a full block is q = 8 (all words, word 7 unmasked).
+        // The length injection is applied with r_eff = r or 0 (identity).
+        if (r || nfull == 2) {
+          const u32 b = nfull ? 8u : 0u;
+          const u32 q = r ? (r >> 2) : 8u;
+          const u32 nleft = r ? (r & 3u) : 4u;
+          u32 P[8];
 #pragma unroll
-            for (u32 j = 0; j < 7; ++j) P[j] = j < q ? Wd[8 * s + j] : 0u;
-            u32 lft = Wd[8 * s + 7];
-#pragma unroll
-            for (u32 j = 0; j < 7; ++j) lft = (q == j) ? Wd[8 * s + j] : lft;
-            P[7] = lft & (nleft >= 4 ? 0xffffffffu : ((1u << (8 * nleft)) - 1u));
-            rem_tweak(h, rem ? r : 0u);
-            h.update(pack(P[0], P[1]), pack(P[2], P[3]), pack(P[4], P[5]), pack(P[6], P[7]));
-          }
+          for (u32 j = 0; j < 7; ++j) P[j] = j < q ? word(b + j) : 0u;
+          const u32 lft = word(b + (q < 7 ? q : 7u));
+          P[7] = lft & (nleft >= 4 ? 0xffffffffu : ((1u << (8 * nleft)) - 1u));
+          rem_tweak(h, r);
+          h.update(pack(P[0], P[1]), pack(P[2], P[3]), pack(P[4], P[5]), pack(P[6], P[7]));
         }
         h.finalize_rounds();
         u64* o64 = out + i * W;
