@@ -172,17 +172,47 @@ struct Highway {
       update(rot32(v0[2]), rot32(v0[3]), rot32(v0[0]), rot32(v0[1]));
   }
 
+  __device__ __forceinline__ void permute_update() {
+    update(rot32(v0[2]), rot32(v0[3]), rot32(v0[0]), rot32(v0[1]));
+  }
+
+  // finalize_rounds + the first W lane sums, with the last two rounds peeled
+  // out of the loop so the compiler drops the state the digest never reads.
+  // W = 1 (HighwayHash-64): out[0] reads lane 0 only, so the last round
+  // needs lanes 0-1 (v1[0] takes the zipper of v0[0], v0[1]) and skips the
+  // second zipper's high word; the round before needs only v0 of lanes 2-3
+  // (the last round's packet is rot32 of v0[2], v0[3]), so their multiplies
+  // and the (2,3) v0 zipper go.  W = 2 drops lanes 2-3 of the last round.
+  // About 70 of ~312 finalization instructions for W = 1.
+  template <int W>
+  __device__ __forceinline__ void finalize_out(u64* out) {
+    int k = rounds;
+    for (; k > 2; --k) permute_update();
+    if (k == 2) permute_update();
+    if (k >= 1) permute_update();
+    out[0] = v0[0] + v1[0] + m0[0] + m1[0];
+    if (W >= 2) out[1] = v0[1] + v1[1] + m0[1] + m1[1];
+    if (W == 4) {
+      out[2] = v0[2] + v1[2] + m0[2] + m1[2];
+      out[3] = v0[3] + v1[3] + m0[3] + m1[3];
+    }
+  }
+
+  // Width dispatch (uniform across a launch: one branch is hot).
+  __device__ __forceinline__ void finalize_out(u64* out) {
+    if (width == 64)
+      finalize_out<1>(out);
+    else if (width == 128)
+      finalize_out<2>(out);
+    else
+      finalize_out<4>(out);
+  }
+
   // Writes width/64 lane sums; lane 0 is HighwayHash-64.
   __device__ __forceinline__ void finish(const u64 (&t)[4], u32 r, u64 /*len*/,
                                          u64* out) {
     if (r) remainder(t, r);
-    finalize_rounds();
-    out[0] = v0[0] + v1[0] + m0[0] + m1[0];
-    if (width >= 128) out[1] = v0[1] + v1[1] + m0[1] + m1[1];
-    if (width == 256) {
-      out[2] = v0[2] + v1[2] + m0[2] + m1[2];
-      out[3] = v0[3] + v1[3] + m0[3] + m1[3];
-    }
+    finalize_out(out);
   }
 };
 

@@ -272,14 +272,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
           rem_tweak(h, r);
           h.update(pack(P[0], P[1]), pack(P[2], P[3]), pack(P[4], P[5]), pack(P[6], P[7]));
         }
-        h.finalize_rounds();
-        u64* o64 = out + i * W;
-        o64[0] = h.v0[0] + h.v1[0] + h.m0[0] + h.m1[0];
-        if (W >= 2) o64[1] = h.v0[1] + h.v1[1] + h.m0[1] + h.m1[1];
-        if (W == 4) {
-          o64[2] = h.v0[2] + h.v1[2] + h.m0[2] + h.m1[2];
-          o64[3] = h.v0[3] + h.v1[3] + h.m0[3] + h.m1[3];
-        }
+        h.finalize_out(out + i * W);
       }
       __syncwarp();
     } else if (valid) {
@@ -598,8 +591,7 @@ __global__ void __launch_bounds__(256) k_prf(const PrfProto proto, u64 start, u6
     zipper(h.v0[0], h.v0[1], z0, z1);
     h.v1[0] = add64_mixed(h.v1[0], z0, h.one);
     h.v1[1] = add64_mixed(h.v1[1], z1, h.one);
-    h.finalize_rounds();
-    out[i] = h.v0[0] + h.v1[0] + h.m0[0] + h.m1[0];
+    h.finalize_out<1>(out + i);
   }
 }
 
