@@ -26,6 +26,7 @@ KERNEL_AUTO = 0
 KERNEL_DIRECT = 1
 KERNEL_TMA = 2
 KERNEL_SPLIT = 3
+KERNEL_STAGED = 4
 
 ALG_HIGHWAY = 0
 ALG_SIPHASH = 1
@@ -47,9 +48,11 @@ def _declare(l):
     l.lh_highway_fixed.argtypes = [vp, u64, u64, vp, i32, i32, vp, vp]
     l.lh_highway_fixed_kernel.argtypes = [vp, u64, u64, vp, i32, i32, vp, vp, i32]
     l.lh_highway_ragged.argtypes = [vp, vp, vp, u64, vp, i32, i32, vp, vp]
+    l.lh_highway_ragged_kernel.argtypes = [vp, vp, vp, u64, vp, i32, i32, vp, vp, i32]
     l.lh_siphash_fixed.argtypes = [vp, u64, u64, vp, i32, i32, i32, vp, vp]
     l.lh_siphash_fixed_kernel.argtypes = [vp, u64, u64, vp, i32, i32, i32, vp, vp, i32]
     l.lh_siphash_ragged.argtypes = [vp, vp, vp, u64, vp, i32, i32, i32, vp, vp]
+    l.lh_siphash_ragged_kernel.argtypes = [vp, vp, vp, u64, vp, i32, i32, i32, vp, vp, i32]
     l.lh_highway_prf64.argtypes = [u64, u64, vp, i32, vp, vp]
     l.lh_stream_state_bytes.argtypes = [i32]
     l.lh_stream_state_bytes.restype = ctypes.c_size_t
@@ -66,7 +69,8 @@ def _declare(l):
     l.lh_sip_round_states.argtypes = [vp, u64, i32, vp]
     for name in (
         "lh_highway_fixed", "lh_highway_fixed_kernel", "lh_highway_ragged",
-        "lh_siphash_fixed", "lh_siphash_fixed_kernel", "lh_siphash_ragged",
+        "lh_highway_ragged_kernel", "lh_siphash_fixed", "lh_siphash_fixed_kernel",
+        "lh_siphash_ragged", "lh_siphash_ragged_kernel",
         "lh_highway_prf64", "lh_synth_fill", "lh_synth_lengths",
         "lh_stream_init", "lh_stream_update", "lh_stream_finish", "lh_avalanche_counts",
         "lh_highway_update_states", "lh_highway_bijectivity",

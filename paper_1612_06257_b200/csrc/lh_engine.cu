@@ -11,6 +11,9 @@
 //       thread pair, 3-D TMA boxes of 16 rows x 512 B per warp.
 //   k_ragged_short  ragged batches of short keys: warp-staged byte spans,
 //       non-divergent Update slots; falls back to the direct reader.
+//   k_ragged_ring<H,D>  ragged batches of medium/long messages (HighwayHash)
+//       and every ragged Sip batch: one thread per message, 32-bit word
+//       reads branch-free in the alignment, D packets in flight.
 //   k_direct<H>  any layout (fixed or ragged, any alignment/length); one
 //       thread per message reading its bytes with 8-byte-aligned loads and
 //       funnel shifts.
@@ -28,6 +31,10 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "../../include/lanehash_b200.h"
 #include "lh_device.cuh"
@@ -171,6 +178,97 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
     }
     H h = proto;
     hash_direct<PF>(h, msg, len, out + i * W);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Ragged medium/long messages when the batch is too small to hide load
+// latency with warps (cfg2: 65,536 messages of 0..1023 bytes, ~14 warps per
+// SM, the longest chain 32 packets).  One thread per message reads 32-bit
+// words and keeps D packets in flight in a register ring (D loads deep
+// instead of one).  The reader is branch-free in the alignment: word m of
+// the message is funnel_r(v[m], v[m+1], s) with s = 8 * (addr & 3) over the
+// 4-byte-aligned word stream starting at addr & ~3 (a zero shift is the
+// identity), so lanes whose messages differ in alignment do not diverge.
+// Word loads are clamped to the last word that holds a message byte (never
+// past the message); a clamped word only feeds a zero shift or masked tail
+// bytes.
+// --------------------------------------------------------------------------
+template <int D, class H>
+__device__ __forceinline__ void hash_ring(H& h, const uint8_t* msg, u64 len, u64* out) {
+  const uintptr_t a = (uintptr_t)msg;
+  const u32* w = (const u32*)(a & ~(uintptr_t)3);
+  const u32 s = (u32)(a & 3) * 8;
+  const u64 nb = len >> 5;
+  const u32 r = (u32)(len & 31);
+  const u64 lastw = len ? ((a + len - 1) >> 2) - (a >> 2) : 0;  // last word with a message byte
+  auto ld = [&](u64 k) { return __ldg(w + (k < lastw ? k : lastw)); };
+  // Words 8*pk+1 .. 8*pk+8 of full packet pk: words up to 8*pk+7 always hold
+  // message bytes (immediate-offset loads), only word 8*pk+8 is clamped.
+  auto ld_packet = [&](u32 (&x)[8], u64 pk) {
+    const u32* p = w + 8 * pk;
+#pragma unroll
+    for (int j = 0; j < 7; ++j) x[j] = __ldg(p + j + 1);
+    x[7] = __ldg(8 * pk + 8 < lastw ? p + 8 : w + lastw);
+  };
+  // ring[k][j] = word 8*(b+k) + j + 1 of the stream; `first` = word 8*b.
+  u32 ring[D][8];
+  u32 first = len ? __ldg(w) : 0u;
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    if ((u64)k < nb) ld_packet(ring[k], (u64)k);
+  auto packet = [&](const u32 (&x)[8], u32& f, u64 (&p)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const u32 lo = __funnelshift_r(j ? x[2 * j - 1] : f, x[2 * j], s);
+      const u32 hi = __funnelshift_r(x[2 * j], x[2 * j + 1], s);
+      p[j] = pack(lo, hi);
+    }
+    f = x[7];
+  };
+  u64 b = 0;
+  for (; b + D <= nb; b += D) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      u64 p[4];
+      packet(ring[k], first, p);
+      if (b + k + D < nb) ld_packet(ring[k], b + k + D);
+      h.absorb32(p);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) {
+    if (b + k < nb) {
+      u64 p[4];
+      packet(ring[k], first, p);
+      h.absorb32(p);
+    }
+  }
+  u64 t[4] = {0, 0, 0, 0};
+  if (r) {
+    // Tail words 8*nb .. 8*nb+8 (clamped), then zero bytes >= r.
+    u32 x[8];
+    const u64 base = 8 * nb;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = ld(base + j + 1);
+    packet(x, first, t);
+    mask_tail(t, r);
+  }
+  h.finish(t, r, len, out);
+}
+
+template <class H, int D>
+__global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_t* __restrict__ buf,
+                                                     const u64* __restrict__ offsets,
+                                                     const u32* __restrict__ lengths, u64 n,
+                                                     u64* __restrict__ out) {
+  const int W = nout(proto);
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x) {
+    const u64 off = offsets[i];
+    const u64 len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
+    H h = proto;
+    hash_ring<D>(h, buf + off, len, out + i * W);
   }
 }
 
@@ -601,15 +699,53 @@ __global__ void __launch_bounds__(256) k_prf(const PrfProto proto, u64 start, u6
 
 int cuda_err(cudaError_t e) { return e == cudaSuccess ? LH_OK : LH_ECUDA; }
 
+// The device checks run on every call; the SM count and the compute
+// capability are cached per device ordinal (idempotent writes, so racing
+// first calls from several host threads agree).
 int check_device(int* sms) {
+  static int cache[128];  // 0 = not yet queried, -1 = unusable, else the SM count
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return LH_ENODEV;
-  int major = 0;
-  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
-    return LH_ENODEV;
-  if (major < 10) return LH_ENODEV;
-  if (sms && cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return LH_ENODEV;
+  int v = (dev >= 0 && dev < 128) ? __atomic_load_n(&cache[dev], __ATOMIC_RELAXED) : 0;
+  if (v == 0) {
+    int major = 0, count = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return LH_ENODEV;
+    v = (major < 10 || count < 1) ? -1 : count;
+    if (dev >= 0 && dev < 128) __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
+  }
+  if (v < 0) return LH_ENODEV;
+  if (sms) *sms = v;
+  return LH_OK;
+}
+
+// cudaFuncSetAttribute (dynamic shared memory) + the occupancy query, once
+// per (kernel, device): both are host round trips that small launch-bound
+// batches would otherwise pay on every call.
+int prepare_kernel(const void* kern, int threads, size_t smem, int* per_sm) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return LH_ENODEV;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find({kern, dev});
+    if (it != cache.end()) {
+      *per_sm = it->second;
+      return LH_OK;
+    }
+  }
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return LH_ECUDA;
+  int v = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, threads, smem) != cudaSuccess ||
+      v < 1)
+    return LH_ECUDA;
+  std::lock_guard<std::mutex> g(mu);
+  cache[{kern, dev}] = v;
+  *per_sm = v;
   return LH_OK;
 }
 
@@ -660,6 +796,25 @@ int launch_direct(const H& proto, const uint8_t* buf, const u64* offsets, const 
   return cuda_err(cudaGetLastError());
 }
 
+// Register-ring reader for ragged batches of medium/long messages
+// (LH_KERNEL_DIRECT on the ragged entry points).
+#ifndef LH_RING_DEPTH
+#define LH_RING_DEPTH 4
+#endif
+constexpr int kRingDepth = LH_RING_DEPTH;
+
+template <class H>
+int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths, u64 n,
+                u64* out, cudaStream_t st) {
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  k_ragged_ring<H, kRingDepth><<<grid_for(n, 128, sms), 128, 0, st>>>(proto, buf, offsets,
+                                                                       lengths, n, out);
+  return cuda_err(cudaGetLastError());
+}
+
 template <class H, int ROWS, int STAGES, int MINB>
 int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                    cudaStream_t st, int sms) {
@@ -667,14 +822,9 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
   if (!enc) return LH_ECUDA;
   constexpr size_t smem = tma_smem_bytes<ROWS, STAGES>();
   auto kern = k_tma_fixed<H, ROWS, STAGES, MINB>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return LH_ECUDA;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ROWS + 32, smem) !=
-          cudaSuccess ||
-      per_sm < 1)
-    return LH_ECUDA;
+  const int prc = prepare_kernel((const void*)kern, ROWS + 32, smem, &per_sm);
+  if (prc) return prc;
   // Rows are split into segments of < 2^31 (TMA coordinates are int32).
   const u64 kSeg = 1ull << 30;
   const int W = nout(proto);
@@ -711,13 +861,9 @@ int launch_split(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64*
   if (!enc) return LH_ECUDA;
   constexpr size_t smem = split_smem_bytes<STAGES, CH>();
   auto kern = k_tma_split<STAGES, CH, MINB>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return LH_ECUDA;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem) != cudaSuccess ||
-      per_sm < 1)
-    return LH_ECUDA;
+  rc = prepare_kernel((const void*)kern, 32, smem, &per_sm);
+  if (rc) return rc;
   const u64 kSeg = 1ull << 30;
   const int W = proto.width / 64;
   for (u64 base = 0; base < n; base += kSeg) {
@@ -814,9 +960,7 @@ bool prefer_split(const H&, const uint8_t*, u64, u64) {
 template <>
 bool prefer_split<Highway>(const Highway&, const uint8_t* msgs, u64 n, u64 len) {
   int sms = 148;
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  check_device(&sms);
   // Few long messages: one thread per message would leave SMs idle; and
   // small-to-medium batches are latency-bound, where halving each thread's
   // Update chain wins (profiles/README.md: 131,072 x 1 KiB 29 us vs 52 us).
@@ -844,7 +988,10 @@ bool valid_width(int w) { return w == 64 || w == 128 || w == 256; }
 template <class H>
 int sip_dispatch_ragged(const H& h, const uint8_t* buf, const u64* off, const u32* lens, u64 n,
                         u64* out, cudaStream_t st) {
-  return launch_direct(h, buf, off, lens, 0, n, out, st);
+  // The register-ring reader is the Sip ragged kernel at every length: its
+  // alignment-branch-free word reads beat the prefetching direct reader even
+  // on short keys (cfg3-shaped SipHash-2-4: 2.86 vs 3.91 ms).
+  return launch_ring(h, buf, off, lens, n, out, st);
 }
 
 }  // namespace
@@ -935,14 +1082,18 @@ int lh_highway_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len, const uint
                                  LH_KERNEL_AUTO);
 }
 
-int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,
-                      uint64_t n, const uint64_t key[4], int width, int rounds, uint64_t* d_out,
-                      void* stream) {
+int lh_highway_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
+                             const uint32_t* d_lengths, uint64_t n, const uint64_t key[4],
+                             int width, int rounds, uint64_t* d_out, void* stream, int kernel) {
   if (!key || !valid_width(width) || rounds < 0 || (n && (!d_out || !d_offsets || !d_buf)))
     return LH_EINVAL;
   if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
     return LH_EALIGN;
+  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT && kernel != LH_KERNEL_STAGED)
+    return LH_EINVAL;
   const Highway h = make_highway(key, width, rounds);
+  if (kernel == LH_KERNEL_DIRECT)
+    return launch_ring(h, d_buf, d_offsets, d_lengths, n, d_out, (cudaStream_t)stream);
   int sms = 0;
   int rc = check_device(&sms);
   if (rc) return rc;
@@ -954,6 +1105,13 @@ int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uin
   k_ragged_short<kWarps><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0,
                            (cudaStream_t)stream>>>(h, d_buf, d_offsets, d_lengths, 0, n, d_out);
   return cuda_err(cudaGetLastError());
+}
+
+int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,
+                      uint64_t n, const uint64_t key[4], int width, int rounds, uint64_t* d_out,
+                      void* stream) {
+  return lh_highway_ragged_kernel(d_buf, d_offsets, d_lengths, n, key, width, rounds, d_out,
+                                  stream, LH_KERNEL_AUTO);
 }
 
 static int sip_fixed_impl(const uint8_t* d_msgs, u64 n, u64 len, const u64 key[2], int c, int d,
@@ -988,12 +1146,13 @@ int lh_siphash_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len, const uint
                                  LH_KERNEL_AUTO);
 }
 
-int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,
-                      uint64_t n, const uint64_t key[2], int c, int d, int tree, uint64_t* d_out,
-                      void* stream) {
+int lh_siphash_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
+                             const uint32_t* d_lengths, uint64_t n, const uint64_t key[2], int c,
+                             int d, int tree, uint64_t* d_out, void* stream, int kernel) {
   if (!key || c < 1 || d < 1 || (n && (!d_out || !d_offsets || !d_buf))) return LH_EINVAL;
   if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
     return LH_EALIGN;
+  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT) return LH_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   if (tree) {
     if (c == 2 && d == 4)
@@ -1013,6 +1172,13 @@ int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uin
                                st);
   return sip_dispatch_ragged(make_sip<0, 0>(key, c, d), d_buf, d_offsets, d_lengths, n, d_out,
                              st);
+}
+
+int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,
+                      uint64_t n, const uint64_t key[2], int c, int d, int tree, uint64_t* d_out,
+                      void* stream) {
+  return lh_siphash_ragged_kernel(d_buf, d_offsets, d_lengths, n, key, c, d, tree, d_out, stream,
+                                  LH_KERNEL_AUTO);
 }
 
 int lh_highway_prf64(uint64_t start, uint64_t n, const uint64_t key[4], int rounds,

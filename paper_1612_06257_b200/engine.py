@@ -29,34 +29,118 @@ import numpy as np
 import torch
 
 from . import _lib
-from .highway import Key256, _check_width, as_key256
-from .sip import Key128, as_key128
+from .highway import Key256, _check_width
+from .highway import as_key256 as _as_key256
+from .sip import Key128
+from .sip import as_key128 as _as_key128
 
 KERNEL_AUTO = _lib.KERNEL_AUTO
 KERNEL_DIRECT = _lib.KERNEL_DIRECT
 KERNEL_TMA = _lib.KERNEL_TMA
 KERNEL_SPLIT = _lib.KERNEL_SPLIT
+KERNEL_STAGED = _lib.KERNEL_STAGED
 
 #: Host-path chunk size (bytes of message payload per H2D copy).
 HOST_CHUNK_BYTES = 128 << 20
+# Ragged batches whose mean message length (buffer bytes / messages) reaches
+# this use the register-ring kernel (KERNEL_DIRECT): several packets in
+# flight per thread; shorter ones the warp-staged short-key kernel.
+RING_MIN_MEAN_BYTES = 128
+
+
+# Per-call host work matters for small, launch-bound batches (cfg1: a 3.5 us
+# kernel): device objects, the raw stream handle and the ctypes key arrays
+# are cached; the device context is only switched when it differs.
+_DEVICES: dict = {}
+_CUDA_CHECKED = False
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
 def _require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise _lib.EngineError("no CUDA device: the B200 engine has no CPU fallback")
-    return torch.device("cuda", torch.cuda.current_device())
+    global _CUDA_CHECKED
+    if not _CUDA_CHECKED:
+        if not torch.cuda.is_available():
+            raise _lib.EngineError("no CUDA device: the B200 engine has no CPU fallback")
+        _CUDA_CHECKED = True
+    i = torch.cuda.current_device()
+    d = _DEVICES.get(i)
+    if d is None:
+        d = _DEVICES[i] = torch.device("cuda", i)
+    return d
 
 
 def _stream_ptr(device) -> int:
+    if _raw_stream is not None:
+        return _raw_stream(device.index if device.index is not None else
+                           torch.cuda.current_device())
     return torch.cuda.current_stream(device).cuda_stream
 
 
+_KEYS: dict = {}
+_KEY_OBJS: dict = {}
+
+
+def _cached_key(key, conv):
+    """Key256/Key128 of a key given as a numpy array or raw bytes, memoised on
+    its bytes (the conversion and validation cost more than a small launch)."""
+    if isinstance(key, (Key256, Key128)):
+        return conv(key)
+    if isinstance(key, np.ndarray):
+        tag = (conv, key.dtype.str, key.tobytes())
+    elif isinstance(key, (bytes, bytearray)):
+        tag = (conv, bytes(key))
+    else:
+        return conv(key)
+    k = _KEY_OBJS.get(tag)
+    if k is None:
+        if len(_KEY_OBJS) > 256:
+            _KEY_OBJS.clear()
+        k = _KEY_OBJS[tag] = conv(key)
+    return k
+
+
+def as_key256(key) -> Key256:
+    return _cached_key(key, _as_key256)
+
+
+def as_key128(key) -> Key128:
+    return _cached_key(key, _as_key128)
+
+
+def _key_array(lanes: tuple):
+    a = _KEYS.get(lanes)
+    if a is None:
+        if len(_KEYS) > 256:
+            _KEYS.clear()
+        a = _KEYS[lanes] = (ctypes.c_uint64 * len(lanes))(*lanes)
+    return a
+
+
 def _key4(key: Key256):
-    return (ctypes.c_uint64 * 4)(*key.lanes)
+    return _key_array(key.lanes)
 
 
 def _key2(key: Key128):
-    return (ctypes.c_uint64 * 2)(key.k0, key.k1)
+    return _key_array((key.k0, key.k1))
+
+
+class _on_device:
+    """torch.cuda.device(d) only when d is not already current."""
+
+    __slots__ = ("ctx",)
+
+    def __init__(self, device):
+        self.ctx = None if device.index == torch.cuda.current_device() else \
+            torch.cuda.device(device)
+
+    def __enter__(self):
+        if self.ctx is not None:
+            self.ctx.__enter__()
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            return self.ctx.__exit__(*exc)
+        return False
 
 
 def to_u64(t) -> np.ndarray:
@@ -120,7 +204,7 @@ def _fixed(kind, key, msgs, p1, p2, tree, lanes, kernel, out=None):
         if out is None:
             out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=m.device)
         if n:
-            with torch.cuda.device(m.device):
+            with _on_device(m.device):
                 _launch_fixed(kind, key, m, n, L, p1, p2, tree, out, kernel, m.device)
         return out
     return _fixed_host(kind, key, m.contiguous(), p1, p2, tree, lanes, kernel, device)
@@ -191,18 +275,34 @@ def _to_device(x, dtype, device):
     ).to(device).contiguous()
 
 
-def _launch_ragged(kind, key, buf_ptr, off_ptr, len_ptr, n, p1, p2, tree, out, device):
+def _ragged_kernel(kind, kernel, span_bytes, n):
+    """Kernel for a ragged launch.  HighwayHash: KERNEL_DIRECT (register
+    ring) when the mean message length reaches RING_MIN_MEAN_BYTES, else the
+    warp-staged short-key kernel.  Sip: always the register ring."""
+    allowed = (KERNEL_DIRECT, KERNEL_STAGED) if kind == "hh" else (KERNEL_DIRECT,)
+    if kernel != KERNEL_AUTO:
+        if kernel not in allowed:
+            raise ValueError(f"ragged {kind} batches take KERNEL_AUTO or one of {allowed}")
+        return kernel
+    if kind != "hh" or (n and span_bytes >= RING_MIN_MEAN_BYTES * n):
+        return KERNEL_DIRECT
+    return KERNEL_STAGED
+
+
+def _launch_ragged(kind, key, buf_ptr, off_ptr, len_ptr, n, p1, p2, tree, out, device,
+                   kernel=KERNEL_AUTO):
     st = _stream_ptr(device)
     if kind == "hh":
-        rc = _lib.lib().lh_highway_ragged(buf_ptr, off_ptr, len_ptr, n, _key4(key), p1, p2,
-                                          out.data_ptr(), st)
+        rc = _lib.lib().lh_highway_ragged_kernel(buf_ptr, off_ptr, len_ptr, n, _key4(key), p1,
+                                                 p2, out.data_ptr(), st, kernel)
     else:
-        rc = _lib.lib().lh_siphash_ragged(buf_ptr, off_ptr, len_ptr, n, _key2(key), p1, p2,
-                                          tree, out.data_ptr(), st)
+        rc = _lib.lib().lh_siphash_ragged_kernel(buf_ptr, off_ptr, len_ptr, n, _key2(key), p1,
+                                                 p2, tree, out.data_ptr(), st, kernel)
     _lib.check(rc, "ragged batch")
 
 
-def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device):
+def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device,
+                           kernel=KERNEL_AUTO):
     """Host ragged batch streamed through the GPU in message-range chunks of
     about HOST_CHUNK_BYTES.  The offsets/lengths go to the device first (one
     copy each); each chunk's byte span [min start, max end) is reduced on the
@@ -259,19 +359,22 @@ def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes
             d_out = torch.empty(_out_shape(b - a, lanes), dtype=torch.int64, device=device)
             _launch_ragged(kind, key, (d_span.data_ptr() - lo) & 0xFFFFFFFFFFFFFFFF,
                            d_o.data_ptr(), None if d_l is None else d_l.data_ptr(), b - a,
-                           p1, p2, tree, d_out, device)
+                           p1, p2, tree, d_out, device, _ragged_kernel(kind, kernel, hi - lo, b - a))
             out_host[a:b].copy_(d_out, non_blocking=True)
     for s in streams:
         s.synchronize()
     return to_u64(out_host)
 
 
-def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None):
+def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
+            kernel=KERNEL_AUTO):
     device = _require_cuda()
+    _ragged_kernel(kind, kernel, 0, 0)  # validate before any work
     host = not (isinstance(buf, torch.Tensor) and buf.is_cuda)
     if host and out is None and not any(isinstance(x, torch.Tensor) and x.is_cuda
                                         for x in (offsets, lengths)):
-        r = _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device)
+        r = _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device,
+                                   kernel)
         if r is not None:
             return r
     if isinstance(offsets, np.ndarray):
@@ -293,29 +396,34 @@ def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None):
     if n:
         bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
         lp = d_len.data_ptr() if d_len is not None else None
-        _launch_ragged(kind, key, bp, d_off.data_ptr(), lp, n, p1, p2, tree, out, device)
+        _launch_ragged(kind, key, bp, d_off.data_ptr(), lp, n, p1, p2, tree, out, device,
+                       _ragged_kernel(kind, kernel, d_buf.numel(), n))
     if host:
         return to_u64(out)
     return out
 
 
 def highway_ragged(key, buf, offsets, lengths=None, width: int = 64, rounds: int = 4,
-                   out: Optional[torch.Tensor] = None):
+                   out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO):
     """HighwayHash over a packed ragged buffer.  Message i is
     buf[offsets[i] : offsets[i] + len_i] with len_i = lengths[i] when given,
-    else offsets[i+1] - offsets[i] (offsets then holds n+1 entries)."""
+    else offsets[i+1] - offsets[i] (offsets then holds n+1 entries).
+    kernel: KERNEL_AUTO picks by mean length (RING_MIN_MEAN_BYTES);
+    KERNEL_DIRECT forces the register-ring kernel, KERNEL_STAGED the
+    warp-staged short-key kernel."""
     _check_width(width)
     if rounds < 0:
         raise ValueError("rounds must be >= 0")
     return _ragged("hh", as_key256(key), buf, offsets, lengths, width, rounds, 0,
-                   width // 64, out)
+                   width // 64, out, kernel)
 
 
 def sip_ragged(key, buf, offsets, lengths=None, c: int = 2, d: int = 4, tree: bool = False,
-               out: Optional[torch.Tensor] = None):
+               out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO):
     if c < 1 or d < 1:
         raise ValueError("round counts must be positive")
-    return _ragged("sip", as_key128(key), buf, offsets, lengths, c, d, int(bool(tree)), 1, out)
+    return _ragged("sip", as_key128(key), buf, offsets, lengths, c, d, int(bool(tree)), 1, out,
+                   kernel)
 
 
 # ---------------------------------------------------------------------------

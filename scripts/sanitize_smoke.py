@@ -44,6 +44,14 @@ check("ragged hh64", engine.highway_ragged(key, buf, off, None, 64),
       oracle.batch_ragged(oracle.ALG_HIGHWAY, key, buf, off, None, 64, 4))
 check("ragged sip13", engine.sip_ragged(k2, buf, off, None, 1, 3),
       oracle.batch_ragged(oracle.ALG_SIPHASH, k2, buf, off, None, 1, 3))
+lens2 = synth.lengths(5, 800, 0, 1500)
+off2 = np.zeros(801, np.uint64)
+off2[1:] = np.cumsum(lens2)
+buf2 = synth.counter_bytes(6, int(off2[-1]))  # last message ends at the allocation's end
+check("ragged ring hh256", engine.highway_ragged(key, buf2, off2, None, 256, kernel=KERNEL_DIRECT),
+      oracle.batch_ragged(oracle.ALG_HIGHWAY, key, buf2, off2, None, 256, 4))
+check("ragged ring tree24", engine.sip_ragged(k2, buf2, off2, None, 2, 4, True, kernel=KERNEL_DIRECT),
+      oracle.batch_ragged(oracle.ALG_SIPTREE, k2, buf2, off2, None, 2, 4))
 check("prf", to_u64(engine.prf64(key, 5, 3000)), oracle.prf64(key, 5, 3000))
 sb = engine.StreamBatch(engine.ALG_HIGHWAY, key, 3000)
 half = off[:-1] + (lens // 2).astype(np.uint64)

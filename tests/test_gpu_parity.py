@@ -16,8 +16,8 @@ import torch
 import paper_1612_06257_b200 as lh
 from conftest import golden_npy
 from paper_1612_06257_b200 import engine, synth
-from paper_1612_06257_b200.engine import (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_SPLIT, KERNEL_TMA,
-                                          to_u64)
+from paper_1612_06257_b200.engine import (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_SPLIT,
+                                          KERNEL_STAGED, KERNEL_TMA, to_u64)
 from paper_1612_06257_b200.highway import Key256
 from paper_1612_06257_b200.sip import SIPHASH_13, SIPHASH_24, Key128, SipParams
 
@@ -344,6 +344,75 @@ def test_ragged_short_paths(oracle, case):
     got = engine.highway_ragged(synth.key256(), buf, off, lens, 64, rounds=2)
     want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, lens, 64, 2)
     assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------------------
+# every ragged kernel on every layout (KERNEL_AUTO picks by mean length)
+# ---------------------------------------------------------------------------
+
+def _ragged_layout(case):
+    rng = np.random.default_rng({"sweep": 21, "long": 22, "scattered": 23, "tiny": 24}[case])
+    if case == "sweep":        # cfg2 shape (small): every length 0..1023 twice, packed
+        lens = np.repeat(np.arange(1024, dtype=np.uint32), 2)
+    elif case == "long":       # ring main loop (>= 2 x 4 packets) plus tails
+        lens = rng.integers(0, 3000, 3000).astype(np.uint32)
+    elif case == "scattered":  # unsorted, overlapping spans
+        lens = rng.integers(0, 1200, 4000).astype(np.uint32)
+    else:                      # short keys, empty messages included
+        lens = rng.integers(0, 70, 9000).astype(np.uint32)
+    if case == "scattered":
+        total = 200000
+        off = rng.integers(0, total - 1200, len(lens)).astype(np.uint64)
+    else:
+        off = np.zeros(len(lens), np.uint64)
+        off[1:] = np.cumsum(lens[:-1])
+        total = int(lens.sum())
+    # The last message ends exactly at the end of the allocation (no read past it).
+    buf = synth.counter_bytes(80, max(total, 1))
+    return buf, off, lens
+
+
+@pytest.mark.parametrize("case", ["sweep", "long", "scattered", "tiny"])
+@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_STAGED])
+def test_ragged_kernels_highway(oracle, case, kernel):
+    buf, off, lens = _ragged_layout(case)
+    d_buf, d_off, d_len = dev(buf), dev(off.view(np.int64)), dev(lens.view(np.int32))
+    for width, rounds in ((64, 4), (128, 4), (256, 4), (64, 0), (64, 1), (256, 2), (64, 5)):
+        got = to_u64(engine.highway_ragged(synth.key256(), d_buf, d_off, d_len, width, rounds,
+                                           kernel=kernel))
+        want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, lens, width,
+                                   rounds)
+        assert np.array_equal(got, want), (case, width, rounds)
+
+
+@pytest.mark.parametrize("shift", [1, 2, 3, 5, 7])
+def test_ragged_ring_unaligned_device_buffer(oracle, shift):
+    buf, off, lens = _ragged_layout("long")
+    raw = np.concatenate([np.full(shift, 0xA5, np.uint8), buf])
+    d_buf = dev(raw)[shift:]
+    got = to_u64(engine.highway_ragged(synth.key256(), d_buf, dev(off.view(np.int64)),
+                                       dev(lens.view(np.int32)), 256, kernel=KERNEL_DIRECT))
+    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf, off, lens, 256, 4)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("case", ["sweep", "long", "tiny"])
+@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT])
+def test_ragged_kernels_sip(oracle, case, kernel):
+    buf, off, lens = _ragged_layout(case)
+    for alg, c, d, tree in ((oracle.ALG_SIPHASH, 2, 4, False), (oracle.ALG_SIPHASH, 1, 3, False),
+                            (oracle.ALG_SIPTREE, 2, 4, True), (oracle.ALG_SIPTREE, 1, 3, True)):
+        got = engine.sip_ragged(synth.key128(), buf, off, lens, c, d, tree, kernel=kernel)
+        want = oracle.batch_ragged(alg, synth.key128(), buf, off, lens, c, d)
+        assert np.array_equal(got, want), (case, c, d, tree)
+
+
+def test_ragged_kernel_choice_rejects_unknown():
+    buf, off, lens = _ragged_layout("tiny")
+    with pytest.raises(ValueError):
+        engine.highway_ragged(synth.key256(), buf, off, lens, kernel=KERNEL_TMA)
+    with pytest.raises(ValueError):
+        engine.sip_ragged(synth.key128(), buf, off, lens, kernel=KERNEL_STAGED)
 
 
 @pytest.mark.parametrize("shift", [1, 3, 8, 13])
