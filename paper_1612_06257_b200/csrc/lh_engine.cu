@@ -12,8 +12,9 @@
 //   k_ragged_short  ragged batches of short keys: warp-staged byte spans,
 //       non-divergent Update slots; falls back to the direct reader.
 //   k_ragged_ring<H,D>  ragged batches of medium/long messages (HighwayHash)
-//       and every ragged Sip batch: one thread per message, 32-bit word
-//       reads branch-free in the alignment, D packets in flight.
+//       and every ragged Sip batch: one thread per message, word reads
+//       branch-free in the alignment (8-byte words for HighwayHash, 4-byte
+//       for Sip), D packets in flight.
 //   k_direct<H>  any layout (fixed or ragged, any alignment/length); one
 //       thread per message reading its bytes with 8-byte-aligned loads and
 //       funnel shifts.
@@ -257,6 +258,89 @@ __device__ __forceinline__ void hash_ring(H& h, const uint8_t* msg, u64 len, u64
   h.finish(t, r, len, out);
 }
 
+// The same reader over 8-byte words (5 loads per packet instead of 9): the
+// byte shift sh = 8 * (addr & 7) is split into a 32-bit word select (sh &
+// 32, per-thread SEL) and a funnel shift by sh & 31, still branch-free.
+template <int D, class H>
+__device__ __forceinline__ void hash_ring64(H& h, const uint8_t* msg, u64 len, u64* out) {
+  const uintptr_t a = (uintptr_t)msg;
+  const u64* w = (const u64*)(a & ~(uintptr_t)7);
+  const u32 sh = (u32)(a & 7) * 8;
+  const bool big = (sh & 32u) != 0;
+  const u32 s5 = sh & 31u;
+  const u64 nb = len >> 5;
+  const u32 r = (u32)(len & 31);
+  const u64 lastw = len ? ((a + len - 1) >> 3) - (a >> 3) : 0;  // last word with a message byte
+  auto ld = [&](u64 k) { return ldg64(w + (k < lastw ? k : lastw)); };
+  // Words 4*pk+1 .. 4*pk+4 of full packet pk; only word 4*pk+4 can lie past
+  // the message (aligned start), so only it is clamped.
+  auto ld_packet = [&](u64 (&x)[4], u64 pk) {
+    const u64* p = w + 4 * pk;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) x[j] = ldg64(p + j + 1);
+    x[3] = ldg64(4 * pk + 4 < lastw ? p + 4 : w + lastw);
+  };
+  // Bytes [sh/8, sh/8 + 8) of hi_w:lo_w.
+  auto fun = [&](u64 lo_w, u64 hi_w) {
+    const u32 x0 = big ? hi32(lo_w) : lo32(lo_w);
+    const u32 x1 = big ? lo32(hi_w) : hi32(lo_w);
+    const u32 x2 = big ? hi32(hi_w) : lo32(hi_w);
+    return pack(__funnelshift_r(x0, x1, s5), __funnelshift_r(x1, x2, s5));
+  };
+  u64 ring[D][4];
+  u64 first = len ? ldg64(w) : 0ull;
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    if ((u64)k < nb) ld_packet(ring[k], (u64)k);
+  auto packet = [&](const u64 (&x)[4], u64& f, u64 (&p)[4]) {
+    p[0] = fun(f, x[0]);
+    p[1] = fun(x[0], x[1]);
+    p[2] = fun(x[1], x[2]);
+    p[3] = fun(x[2], x[3]);
+    f = x[3];
+  };
+  u64 b = 0;
+  for (; b + D <= nb; b += D) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      u64 p[4];
+      packet(ring[k], first, p);
+      if (b + k + D < nb) ld_packet(ring[k], b + k + D);
+      h.absorb32(p);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) {
+    if (b + k < nb) {
+      u64 p[4];
+      packet(ring[k], first, p);
+      h.absorb32(p);
+    }
+  }
+  u64 t[4] = {0, 0, 0, 0};
+  if (r) {
+    u64 x[4];
+    const u64 base = 4 * nb;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = ld(base + j + 1);
+    packet(x, first, t);
+    mask_tail(t, r);
+  }
+  h.finish(t, r, len, out);
+}
+
+// 8-byte words for HighwayHash (cfg2 26.6 -> 22.5 us; 4 GiB of 512..1536-B
+// messages 1.72 -> 1.33 ms); 4-byte words for the Sip family, whose extra
+// ALU work makes the 64-bit form's selects cost more than the loads it saves.
+template <class H>
+struct RingWide {
+  static constexpr bool value = false;
+};
+template <>
+struct RingWide<Highway> {
+  static constexpr bool value = true;
+};
+
 template <class H, int D>
 __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_t* __restrict__ buf,
                                                      const u64* __restrict__ offsets,
@@ -268,7 +352,10 @@ __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_
     const u64 off = offsets[i];
     const u64 len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
     H h = proto;
-    hash_ring<D>(h, buf + off, len, out + i * W);
+    if constexpr (RingWide<H>::value)
+      hash_ring64<D>(h, buf + off, len, out + i * W);
+    else
+      hash_ring<D>(h, buf + off, len, out + i * W);
   }
 }
 
