@@ -49,7 +49,10 @@ extern "C" {
 #define LH_KERNEL_TMA 2    /* TMA-staged shared-memory ring (fixed length) */
 #define LH_KERNEL_SPLIT 3  /* HighwayHash only: state split over 2 threads per
                               message (long messages; len % 128 == 0) */
-#define LH_KERNEL_STAGED 4 /* ragged HighwayHash: warp-staged short-key kernel */
+#define LH_KERNEL_STAGED 4 /* HighwayHash: warp-staged short-key kernel
+                              (ragged, or fixed rows) */
+#define LH_KERNEL_RING 5   /* one thread per message, branch-free word reader
+                              with 4 packets in flight (fixed or ragged) */
 
 /* Library / build identification. */
 const char* lh_version(void);
@@ -80,9 +83,9 @@ int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets,
 /* kernel: LH_KERNEL_AUTO or LH_KERNEL_STAGED = warp-staged short-key kernel
  * (messages <= 64 B packed together; any other warp reads its messages
  * directly);
- * LH_KERNEL_DIRECT = one thread per message with a register ring of 4
- * packets in flight (medium/long messages in batches too small to hide load
- * latency with warps, e.g. the L = 0..1023 sweep). */
+ * LH_KERNEL_RING (or LH_KERNEL_DIRECT) = one thread per message with a
+ * register ring of 4 packets in flight (medium/long messages, e.g. the
+ * L = 0..1023 sweep). */
 int lh_highway_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
                              const uint32_t* d_lengths, uint64_t n,
                              const uint64_t key[4], int width, int rounds,
@@ -101,8 +104,9 @@ int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets,
                       const uint32_t* d_lengths, uint64_t n,
                       const uint64_t key[2], int c, int d, int tree,
                       uint64_t* d_out, void* stream);
-/* kernel: LH_KERNEL_AUTO or LH_KERNEL_DIRECT (the same kernel: one thread
- * per message, the register-ring reader described above). */
+/* kernel: LH_KERNEL_AUTO, LH_KERNEL_RING or LH_KERNEL_DIRECT (the same
+ * kernel: one thread per message, the register-ring reader described
+ * above). */
 int lh_siphash_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
                              const uint32_t* d_lengths, uint64_t n,
                              const uint64_t key[2], int c, int d, int tree,

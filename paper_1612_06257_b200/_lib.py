@@ -27,6 +27,7 @@ KERNEL_DIRECT = 1
 KERNEL_TMA = 2
 KERNEL_SPLIT = 3
 KERNEL_STAGED = 4
+KERNEL_RING = 5
 
 ALG_HIGHWAY = 0
 ALG_SIPHASH = 1

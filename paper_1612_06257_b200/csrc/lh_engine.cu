@@ -344,13 +344,20 @@ struct RingWide<Highway> {
 template <class H, int D>
 __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_t* __restrict__ buf,
                                                      const u64* __restrict__ offsets,
-                                                     const u32* __restrict__ lengths, u64 n,
+                                                     const u32* __restrict__ lengths,
+                                                     u64 fixed_len, u64 n,
                                                      u64* __restrict__ out) {
   const int W = nout(proto);
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (u64)gridDim.x * blockDim.x) {
-    const u64 off = offsets[i];
-    const u64 len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
+    u64 off, len;
+    if (offsets) {
+      off = offsets[i];
+      len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
+    } else {  // fixed layout: message i = buf[i*L : (i+1)*L]
+      off = i * fixed_len;
+      len = fixed_len;
+    }
     H h = proto;
     if constexpr (RingWide<H>::value)
       hash_ring64<D>(h, buf + off, len, out + i * W);
@@ -891,14 +898,30 @@ int launch_direct(const H& proto, const uint8_t* buf, const u64* offsets, const 
 constexpr int kRingDepth = LH_RING_DEPTH;
 
 template <class H>
-int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths, u64 n,
-                u64* out, cudaStream_t st) {
+int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths,
+                u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
   int sms = 0;
   int rc = check_device(&sms);
   if (rc) return rc;
   if (n == 0) return LH_OK;
-  k_ragged_ring<H, kRingDepth><<<grid_for(n, 128, sms), 128, 0, st>>>(proto, buf, offsets,
-                                                                       lengths, n, out);
+  k_ragged_ring<H, kRingDepth><<<grid_for(n, 128, sms), 128, 0, st>>>(
+      proto, buf, offsets, lengths, fixed_len, n, out);
+  return cuda_err(cudaGetLastError());
+}
+
+// Warp-staged short-key kernel (HighwayHash only), ragged or fixed layout.
+int launch_staged(const Highway& proto, const uint8_t* buf, const u64* offsets,
+                  const u32* lengths, u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  constexpr int kWarps = 8;
+  const u64 warps = (n + 31) / 32;
+  const u64 cap = (u64)sms * 8 * (64 / kWarps);
+  const u64 blocks = (warps + kWarps - 1) / kWarps;
+  k_ragged_short<kWarps><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0, st>>>(
+      proto, buf, offsets, lengths, fixed_len, n, out);
   return cuda_err(cudaGetLastError());
 }
 
@@ -1056,6 +1079,32 @@ bool prefer_split<Highway>(const Highway&, const uint8_t* msgs, u64 n, u64 len) 
 }
 
 template <class H>
+int dispatch_staged(const H&, const uint8_t*, u64, u64, u64*, cudaStream_t) {
+  return LH_EINVAL;  // the warp-staged kernel is HighwayHash only
+}
+template <>
+int dispatch_staged<Highway>(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
+                             cudaStream_t st) {
+  return launch_staged(proto, msgs, nullptr, nullptr, len, n, out, st);
+}
+
+// Fixed-length batches the TMA kernel does not take (row length not a
+// multiple of 16, or < 1,024 rows).  HighwayHash (scripts/untiled_ab.py,
+// DESIGN.md §9): rows of <= 64 bytes -> warp-staged kernel, longer rows ->
+// register ring (1.2-1.8x the direct reader).  Sip: the direct reader.
+template <class H>
+int dispatch_untiled(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
+                     cudaStream_t st) {
+  return launch_direct(proto, msgs, nullptr, nullptr, len, n, out, st);
+}
+template <>
+int dispatch_untiled<Highway>(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
+                              cudaStream_t st) {
+  if (len <= 64) return launch_staged(proto, msgs, nullptr, nullptr, len, n, out, st);
+  return launch_ring(proto, msgs, nullptr, nullptr, len, n, out, st);
+}
+
+template <class H>
 int dispatch_fixed(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                    cudaStream_t st, int kernel) {
   if (kernel == LH_KERNEL_SPLIT) return n ? dispatch_split(proto, msgs, n, len, out, st) : LH_OK;
@@ -1065,8 +1114,11 @@ int dispatch_fixed(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
     if (n && !tma_ok(msgs, n, len)) return LH_EINVAL;
     return launch_tma(proto, msgs, n, len, out, st);
   }
+  if (kernel == LH_KERNEL_RING) return launch_ring(proto, msgs, nullptr, nullptr, len, n, out, st);
+  if (kernel == LH_KERNEL_STAGED) return dispatch_staged(proto, msgs, n, len, out, st);
   if (kernel == LH_KERNEL_AUTO && tma_ok(msgs, n, len) && n >= 1024)
     return launch_tma(proto, msgs, n, len, out, st);
+  if (kernel == LH_KERNEL_AUTO) return dispatch_untiled(proto, msgs, n, len, out, st);
   return launch_direct(proto, msgs, nullptr, nullptr, len, n, out, st);
 }
 
@@ -1078,7 +1130,7 @@ int sip_dispatch_ragged(const H& h, const uint8_t* buf, const u64* off, const u3
   // The register-ring reader is the Sip ragged kernel at every length: its
   // alignment-branch-free word reads beat the prefetching direct reader even
   // on short keys (cfg3-shaped SipHash-2-4: 2.86 vs 3.91 ms).
-  return launch_ring(h, buf, off, lens, n, out, st);
+  return launch_ring(h, buf, off, lens, 0, n, out, st);
 }
 
 }  // namespace
@@ -1157,7 +1209,7 @@ int lh_highway_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
   if (!key || !valid_width(width) || rounds < 0 || (n && !d_out) || (n && len && !d_msgs))
     return LH_EINVAL;
   if ((uintptr_t)d_out % 8) return LH_EALIGN;
-  if (kernel < 0 || kernel > LH_KERNEL_SPLIT) return LH_EINVAL;
+  if (kernel < 0 || kernel > LH_KERNEL_RING) return LH_EINVAL;
   if (len && n > UINT64_MAX / len) return LH_ETOOBIG;
   const Highway h = make_highway(key, width, rounds);
   return dispatch_fixed(h, d_msgs, n, len, d_out, (cudaStream_t)stream, kernel);
@@ -1176,22 +1228,13 @@ int lh_highway_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
     return LH_EINVAL;
   if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
     return LH_EALIGN;
-  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT && kernel != LH_KERNEL_STAGED)
+  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT && kernel != LH_KERNEL_STAGED &&
+      kernel != LH_KERNEL_RING)
     return LH_EINVAL;
   const Highway h = make_highway(key, width, rounds);
-  if (kernel == LH_KERNEL_DIRECT)
-    return launch_ring(h, d_buf, d_offsets, d_lengths, n, d_out, (cudaStream_t)stream);
-  int sms = 0;
-  int rc = check_device(&sms);
-  if (rc) return rc;
-  if (n == 0) return LH_OK;
-  constexpr int kWarps = 8;
-  const u64 warps = (n + 31) / 32;
-  const u64 cap = (u64)sms * 8 * (64 / kWarps);
-  const u64 blocks = (warps + kWarps - 1) / kWarps;
-  k_ragged_short<kWarps><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0,
-                           (cudaStream_t)stream>>>(h, d_buf, d_offsets, d_lengths, 0, n, d_out);
-  return cuda_err(cudaGetLastError());
+  if (kernel == LH_KERNEL_DIRECT || kernel == LH_KERNEL_RING)
+    return launch_ring(h, d_buf, d_offsets, d_lengths, 0, n, d_out, (cudaStream_t)stream);
+  return launch_staged(h, d_buf, d_offsets, d_lengths, 0, n, d_out, (cudaStream_t)stream);
 }
 
 int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,
@@ -1222,7 +1265,9 @@ int lh_siphash_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
                             void* stream, int kernel) {
   if (!key || c < 1 || d < 1 || (n && !d_out) || (n && len && !d_msgs)) return LH_EINVAL;
   if ((uintptr_t)d_out % 8) return LH_EALIGN;
-  if (kernel < 0 || kernel > LH_KERNEL_TMA) return LH_EINVAL;
+  if (kernel < 0 || kernel > LH_KERNEL_RING || kernel == LH_KERNEL_SPLIT ||
+      kernel == LH_KERNEL_STAGED)
+    return LH_EINVAL;
   if (len && n > UINT64_MAX / len) return LH_ETOOBIG;
   return sip_fixed_impl(d_msgs, n, len, key, c, d, tree, d_out, (cudaStream_t)stream, kernel);
 }
@@ -1239,7 +1284,8 @@ int lh_siphash_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
   if (!key || c < 1 || d < 1 || (n && (!d_out || !d_offsets || !d_buf))) return LH_EINVAL;
   if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
     return LH_EALIGN;
-  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT) return LH_EINVAL;
+  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT && kernel != LH_KERNEL_RING)
+    return LH_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   if (tree) {
     if (c == 2 && d == 4)

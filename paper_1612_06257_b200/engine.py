@@ -39,12 +39,13 @@ KERNEL_DIRECT = _lib.KERNEL_DIRECT
 KERNEL_TMA = _lib.KERNEL_TMA
 KERNEL_SPLIT = _lib.KERNEL_SPLIT
 KERNEL_STAGED = _lib.KERNEL_STAGED
+KERNEL_RING = _lib.KERNEL_RING
 
 #: Host-path chunk size (bytes of message payload per H2D copy).
 HOST_CHUNK_BYTES = 128 << 20
 # Ragged batches whose mean message length (buffer bytes / messages) reaches
-# this use the register-ring kernel (KERNEL_DIRECT): several packets in
-# flight per thread; shorter ones the warp-staged short-key kernel.
+# this use the register-ring kernel (KERNEL_RING): several packets in flight
+# per thread; shorter ones the warp-staged short-key kernel.
 RING_MIN_MEAN_BYTES = 128
 
 
@@ -279,13 +280,14 @@ def _ragged_kernel(kind, kernel, span_bytes, n):
     """Kernel for a ragged launch.  HighwayHash: KERNEL_DIRECT (register
     ring) when the mean message length reaches RING_MIN_MEAN_BYTES, else the
     warp-staged short-key kernel.  Sip: always the register ring."""
-    allowed = (KERNEL_DIRECT, KERNEL_STAGED) if kind == "hh" else (KERNEL_DIRECT,)
+    allowed = (KERNEL_DIRECT, KERNEL_RING, KERNEL_STAGED) if kind == "hh" else \
+        (KERNEL_DIRECT, KERNEL_RING)
     if kernel != KERNEL_AUTO:
         if kernel not in allowed:
             raise ValueError(f"ragged {kind} batches take KERNEL_AUTO or one of {allowed}")
         return kernel
     if kind != "hh" or (n and span_bytes >= RING_MIN_MEAN_BYTES * n):
-        return KERNEL_DIRECT
+        return KERNEL_RING
     return KERNEL_STAGED
 
 
@@ -409,8 +411,8 @@ def highway_ragged(key, buf, offsets, lengths=None, width: int = 64, rounds: int
     buf[offsets[i] : offsets[i] + len_i] with len_i = lengths[i] when given,
     else offsets[i+1] - offsets[i] (offsets then holds n+1 entries).
     kernel: KERNEL_AUTO picks by mean length (RING_MIN_MEAN_BYTES);
-    KERNEL_DIRECT forces the register-ring kernel, KERNEL_STAGED the
-    warp-staged short-key kernel."""
+    KERNEL_RING (or KERNEL_DIRECT) forces the register-ring kernel,
+    KERNEL_STAGED the warp-staged short-key kernel."""
     _check_width(width)
     if rounds < 0:
         raise ValueError("rounds must be >= 0")

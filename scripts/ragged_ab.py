@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""A/B of the ragged kernels (KERNEL_STAGED vs KERNEL_DIRECT register ring)
+"""A/B of the ragged kernels (KERNEL_STAGED vs KERNEL_RING register ring)
 on ragged shapes: the cfg2 sweep, the cfg3 short keys, and medium/long
 random lengths.  CUDA-event median per launch, device-resident inputs."""
 import json
@@ -13,7 +13,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1612_06257_b200 import engine, synth  # noqa: E402
-from paper_1612_06257_b200.engine import KERNEL_DIRECT, KERNEL_STAGED  # noqa: E402
+from paper_1612_06257_b200.engine import KERNEL_RING, KERNEL_STAGED  # noqa: E402
 
 
 def med(fn, steps=30, warmup=5):
@@ -60,7 +60,7 @@ def main():
         o = torch.empty(n, dtype=torch.int64, device="cuda")
         res = {"shape": name, "n": n, "bytes": total}
         ref = None
-        for kname, k in (("staged", KERNEL_STAGED), ("ring", KERNEL_DIRECT)):
+        for kname, k in (("staged", KERNEL_STAGED), ("ring", KERNEL_RING)):
             ms = med(lambda: engine.highway_ragged(key, d_b, d_off, d_len, 64, out=o, kernel=k))
             res[kname + "_ms"] = round(ms, 4)
             res[kname + "_GBs"] = round(total / ms / 1e6, 1)
@@ -68,7 +68,7 @@ def main():
                 ref = o.clone()
             else:
                 res["agree"] = bool(torch.equal(ref, o))
-        for kname, k in (("sip24_auto", engine.KERNEL_AUTO), ("sip24_ring", KERNEL_DIRECT)):
+        for kname, k in (("sip24_auto", engine.KERNEL_AUTO), ("sip24_ring", KERNEL_RING)):
             ms = med(lambda: engine.sip_ragged(synth.key128(), d_b, d_off, d_len, 2, 4, out=o,
                                                kernel=k), steps=10, warmup=2)
             res[kname + "_ms"] = round(ms, 4)

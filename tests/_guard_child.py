@@ -22,8 +22,8 @@ import torch  # noqa: E402
 
 from oracle import oracle  # noqa: E402
 from paper_1612_06257_b200 import _lib, synth  # noqa: E402
-from paper_1612_06257_b200.engine import (KERNEL_DIRECT, KERNEL_SPLIT, KERNEL_STAGED,  # noqa: E402
-                                          KERNEL_TMA)
+from paper_1612_06257_b200.engine import (KERNEL_DIRECT, KERNEL_RING, KERNEL_SPLIT,  # noqa: E402
+                                          KERNEL_STAGED, KERNEL_TMA)
 
 cu = ctypes.CDLL("libcuda.so.1")
 u64, sz, vp = ctypes.c_uint64, ctypes.c_size_t, ctypes.c_void_p
@@ -120,13 +120,13 @@ def main(mode: str) -> int:
         m = synth.counter_bytes(L + 1, n * L).reshape(n, L)
         p = put(m, at_end)
         want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, m, 256, 4)
-        kernels = [KERNEL_DIRECT] + ([KERNEL_TMA] if L % 16 == 0 else []) + \
-            ([KERNEL_SPLIT] if L % 128 == 0 else [])
+        kernels = [KERNEL_DIRECT, KERNEL_RING] + ([KERNEL_TMA] if L % 16 == 0 else []) + \
+            ([KERNEL_SPLIT] if L % 128 == 0 else []) + ([KERNEL_STAGED] if L <= 64 else [])
         for kern in kernels:
             run(f"hh256 n={n} L={L} k={kern}",
                 lambda o: lib.lh_highway_fixed_kernel(p, n, L, k4, 256, 4, o, st, kern), n, 4, want)
         want = oracle.batch_fixed(oracle.ALG_SIPTREE, synth.key128(), m, 2, 4)
-        for kern in [KERNEL_DIRECT] + ([KERNEL_TMA] if L % 16 == 0 else []):
+        for kern in [KERNEL_DIRECT, KERNEL_RING] + ([KERNEL_TMA] if L % 16 == 0 else []):
             run(f"tree24 n={n} L={L} k={kern}",
                 lambda o: lib.lh_siphash_fixed_kernel(p, n, L, k2, 2, 4, 1, o, st, kern), n, 1,
                 want)
@@ -142,7 +142,7 @@ def main(mode: str) -> int:
         p = put(buf, at_end)
         d_off = torch.from_numpy(off.view(np.int64)).cuda()
         n = len(lens)
-        for kern in (KERNEL_STAGED, KERNEL_DIRECT):
+        for kern in (KERNEL_STAGED, KERNEL_RING):
             want = oracle.batch_ragged(oracle.ALG_HIGHWAY, key, buf, off, None, 64, 4)
             run(f"ragged hh64 {name} k={kern}",
                 lambda o: lib.lh_highway_ragged_kernel(p, d_off.data_ptr(), None, n, k4, 64, 4, o,

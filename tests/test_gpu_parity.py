@@ -16,7 +16,7 @@ import torch
 import paper_1612_06257_b200 as lh
 from conftest import golden_npy
 from paper_1612_06257_b200 import engine, synth
-from paper_1612_06257_b200.engine import (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_SPLIT,
+from paper_1612_06257_b200.engine import (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING, KERNEL_SPLIT,
                                           KERNEL_STAGED, KERNEL_TMA, to_u64)
 from paper_1612_06257_b200.highway import Key256
 from paper_1612_06257_b200.sip import SIPHASH_13, SIPHASH_24, Key128, SipParams
@@ -84,7 +84,7 @@ def test_sip_cases(golden):
 # cfg1: 4096 x 1 KiB, both kernels, host and device entry
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_TMA])
+@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_TMA, KERNEL_RING])
 def test_cfg1_kernels(kernel):
     key = synth.key256()
     msgs = synth.numpy_bytes(1, (4096, 1024))
@@ -114,6 +114,29 @@ def test_cfg1_widths_vs_oracle(oracle, width, kernel):
     want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, msgs, width, 4)
     got = to_u64(engine.highway_batch(key, dev(msgs), width, 4, kernel=kernel))
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("L", [0, 1, 8, 15, 16, 17, 31, 32, 33, 47, 48, 63, 64, 65, 100, 1000,
+                               1023, 4095])
+def test_fixed_rows_every_kernel(oracle, L):
+    """Fixed-length rows through the direct, ring and (rows of <= 64 B)
+    staged kernels and KERNEL_AUTO's choice for non-TMA shapes."""
+    key = synth.key256()
+    n = 3000 if L <= 1024 else 300
+    msgs = synth.counter_bytes(90 + L, n * L).reshape(n, L)
+    d = dev(msgs)
+    kernels = [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING] + ([KERNEL_STAGED] if L <= 64 else [])
+    for width, rounds in ((64, 4), (256, 4), (128, 1), (64, 0)):
+        want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, msgs, width, rounds)
+        for kernel in kernels:
+            got = to_u64(engine.highway_batch(key, d, width, rounds, kernel=kernel))
+            assert np.array_equal(got, want), (L, kernel, width, rounds)
+    want = oracle.batch_fixed(oracle.ALG_SIPTREE, synth.key128(), msgs, 2, 4)
+    for kernel in (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING):
+        got = to_u64(engine.sip_batch(synth.key128(), d, 2, 4, True, kernel=kernel))
+        assert np.array_equal(got, want), (L, kernel)
+    with pytest.raises(ValueError):
+        engine.sip_batch(synth.key128(), d, 2, 4, kernel=KERNEL_STAGED)
 
 
 @pytest.mark.parametrize("rounds", [0, 1, 2, 3, 5])
@@ -373,7 +396,7 @@ def _ragged_layout(case):
 
 
 @pytest.mark.parametrize("case", ["sweep", "long", "scattered", "tiny"])
-@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_STAGED])
+@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING, KERNEL_STAGED])
 def test_ragged_kernels_highway(oracle, case, kernel):
     buf, off, lens = _ragged_layout(case)
     d_buf, d_off, d_len = dev(buf), dev(off.view(np.int64)), dev(lens.view(np.int32))

@@ -12,8 +12,8 @@ import pytest
 import torch
 
 from paper_1612_06257_b200 import engine, synth
-from paper_1612_06257_b200.engine import (KERNEL_DIRECT, KERNEL_SPLIT, KERNEL_STAGED, KERNEL_TMA,
-                                          to_u64)
+from paper_1612_06257_b200.engine import (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING, KERNEL_SPLIT,
+                                          KERNEL_STAGED, KERNEL_TMA, to_u64)
 
 pytestmark = pytest.mark.gpu
 
@@ -54,7 +54,7 @@ def test_random_ragged(oracle, seed):
         width = int(rng.choice([64, 128, 256]))
         rounds = int(rng.integers(0, 6))
         want = oracle.batch_ragged(oracle.ALG_HIGHWAY, key, buf, off, lens, width, rounds)
-        for kernel in (KERNEL_STAGED, KERNEL_DIRECT):
+        for kernel in (KERNEL_STAGED, KERNEL_RING):
             got = to_u64(engine.highway_ragged(key, d_buf, d_off, d_len, width, rounds,
                                                kernel=kernel))
             assert np.array_equal(got, want), (seed, kernel, width, rounds, len(lens))
@@ -79,11 +79,14 @@ def test_random_fixed(oracle, seed):
         width = int(rng.choice([64, 128, 256]))
         rounds = int(rng.integers(0, 6))
         want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, m, width, rounds)
-        kernels = [KERNEL_DIRECT]
+        sip_kernels = [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING]
         if L >= 32 and L % 16 == 0:
-            kernels.append(KERNEL_TMA)
+            sip_kernels.append(KERNEL_TMA)
+        kernels = list(sip_kernels)
         if L >= 128 and L % 128 == 0:
             kernels.append(KERNEL_SPLIT)
+        if L <= 64:
+            kernels.append(KERNEL_STAGED)
         for kernel in kernels:
             got = to_u64(engine.highway_batch(key, d, width, rounds, kernel=kernel))
             assert np.array_equal(got, want), (seed, kernel, n, L, width, rounds)
@@ -91,6 +94,6 @@ def test_random_fixed(oracle, seed):
         tree = bool(rng.integers(0, 2))
         alg = oracle.ALG_SIPTREE if tree else oracle.ALG_SIPHASH
         want = oracle.batch_fixed(alg, k2, m, c, dd)
-        for kernel in kernels[:2]:
+        for kernel in sip_kernels:
             got = to_u64(engine.sip_batch(k2, d, c, dd, tree, kernel=kernel))
             assert np.array_equal(got, want), (seed, kernel, n, L, c, dd, tree)
