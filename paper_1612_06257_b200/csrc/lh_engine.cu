@@ -1088,20 +1088,25 @@ int dispatch_staged<Highway>(const Highway& proto, const uint8_t* msgs, u64 n, u
   return launch_staged(proto, msgs, nullptr, nullptr, len, n, out, st);
 }
 
-// Fixed-length batches the TMA kernel does not take (row length not a
-// multiple of 16, or < 1,024 rows).  HighwayHash (scripts/untiled_ab.py,
-// DESIGN.md §9): rows of <= 64 bytes -> warp-staged kernel, longer rows ->
-// register ring (1.2-1.8x the direct reader).  Sip: the direct reader.
+// Fixed-length batches the TMA kernel does not take: rows whose length is
+// not a multiple of 16 (so rows start at every alignment), or fewer than
+// 1,024 rows (latency-bound).  Measured (scripts/untiled_ab.py, DESIGN.md
+// §9): unaligned rows go to the register ring (HighwayHash 1.2-1.8x, Sip
+// 1.4-2.2x the direct reader, whose alignment branches diverge); HighwayHash
+// rows of <= 64 bytes to the warp-staged kernel; 16-byte-multiple rows of a
+// small batch keep the direct reader (16-byte loads, next-packet prefetch).
 template <class H>
 int dispatch_untiled(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                      cudaStream_t st) {
+  if (len > 32 && len % 16) return launch_ring(proto, msgs, nullptr, nullptr, len, n, out, st);
   return launch_direct(proto, msgs, nullptr, nullptr, len, n, out, st);
 }
 template <>
 int dispatch_untiled<Highway>(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                               cudaStream_t st) {
   if (len <= 64) return launch_staged(proto, msgs, nullptr, nullptr, len, n, out, st);
-  return launch_ring(proto, msgs, nullptr, nullptr, len, n, out, st);
+  if (len % 16) return launch_ring(proto, msgs, nullptr, nullptr, len, n, out, st);
+  return launch_direct(proto, msgs, nullptr, nullptr, len, n, out, st);
 }
 
 template <class H>
