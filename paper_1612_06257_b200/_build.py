@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libb200hash.so")
 SOURCES = ["lh_engine.cu", "lh_synth.cu", "lh_stream.cu", "lh_quality.cu", "lh_state.cu"]
-HEADERS = ["lh_device.cuh", "lh_tma.cuh", "lh_reader.cuh", "lh_host.cuh", "lh_mix.cuh"]
+HEADERS = ["lh_device.cuh", "lh_tma.cuh", "lh_reader.cuh", "lh_host.cuh", "lh_mix.cuh",
+           "lh_stream.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

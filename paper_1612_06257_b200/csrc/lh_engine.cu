@@ -41,6 +41,7 @@
 #include "lh_device.cuh"
 #include "lh_reader.cuh"
 #include "lh_host.cuh"
+#include "lh_stream.cuh"
 #include "lh_tma.cuh"
 
 using namespace lh;
@@ -497,10 +498,15 @@ constexpr size_t tma_smem_bytes() {
   return 1024 /*alignment slack*/ + (size_t)STAGES * ROWS * kBoxBytes + 2 * STAGES * 8;
 }
 
-template <class H, int ROWS, int STAGES, int MINB>
+// STREAM: the streaming append of whole-block chunks (lh_stream_update):
+// each row starts from its StreamRec's state instead of the prototype and
+// stores the state back instead of finishing; a row with a pending tail
+// (not block-aligned) takes the generic append from global memory.
+template <class H, int ROWS, int STAGES, int MINB, bool STREAM = false>
 __global__ void __launch_bounds__(ROWS + 32, MINB)
     k_tma_fixed(const __grid_constant__ CUtensorMap tmap, const H proto, u64 n, u64 len,
-                u64* __restrict__ out, u32 pf) {
+                u64* __restrict__ out, u32 pf, StreamRec<H>* __restrict__ rec,
+                const uint8_t* __restrict__ chunks) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr u32 kStageBytes = ROWS * kBoxBytes;
@@ -590,7 +596,15 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   asm volatile("mov.b32 %0, %1;" : "=r"(bars) : "r"(smem_u32(full_bar)));
   u32 used = 0;
   for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const u64 row_idx = tile * ROWS + t;
     H h = proto;
+    bool fast = true;
+    if constexpr (STREAM) {
+      if (row_idx < n) {
+        h = rec[row_idx].h;
+        fast = rec[row_idx].tlen == 0;
+      }
+    }
     u64 tl[4] = {0, 0, 0, 0};
     for (u32 cb = 0; cb < nchunks; cb += STAGES) {
 #pragma unroll
@@ -605,7 +619,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
               const uint4 a = lds128(ua[2 * k] + ss * kStageBytes);
               const uint4 b = lds128(ua[2 * k + 1] + ss * kStageBytes);
               const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
-              h.absorb32(p);
+              if (!STREAM || fast) h.absorb32(p);
             }
           } else {
             // Last chunk of a message whose length is not a multiple of
@@ -616,7 +630,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
               const uint4 a = lds128(rowa + (((2 * k) ^ sw) << 4));
               const uint4 b = lds128(rowa + (((2 * k + 1) ^ sw) << 4));
               const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
-              h.absorb32(p);
+              if (!STREAM || fast) h.absorb32(p);
             }
             if (r) {
               const uint4 a = lds128(rowa + (((2 * kvalid) ^ sw) << 4));
@@ -629,8 +643,20 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
         }
       }
     }
-    const u64 row_idx = tile * ROWS + t;
-    if (row_idx < n) h.finish(tl, r, len, out + row_idx * W);
+    if constexpr (STREAM) {
+      if (row_idx < n) {
+        if (fast) {
+          rec[row_idx].h = h;
+          rec[row_idx].total += len;
+        } else {
+          StreamRec<H> rr = rec[row_idx];
+          stream_append(rr, chunks + row_idx * len, len);
+          rec[row_idx] = rr;
+        }
+      }
+    } else {
+      if (row_idx < n) h.finish(tl, r, len, out + row_idx * W);
+    }
   }
 }
 
@@ -925,13 +951,13 @@ int launch_staged(const Highway& proto, const uint8_t* buf, const u64* offsets,
   return cuda_err(cudaGetLastError());
 }
 
-template <class H, int ROWS, int STAGES, int MINB>
+template <class H, int ROWS, int STAGES, int MINB, bool STREAM = false>
 int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
-                   cudaStream_t st, int sms) {
+                   cudaStream_t st, int sms, StreamRec<H>* rec = nullptr) {
   auto enc = get_encode();
   if (!enc) return LH_ECUDA;
   constexpr size_t smem = tma_smem_bytes<ROWS, STAGES>();
-  auto kern = k_tma_fixed<H, ROWS, STAGES, MINB>;
+  auto kern = k_tma_fixed<H, ROWS, STAGES, MINB, STREAM>;
   int per_sm = 0;
   const int prc = prepare_kernel((const void*)kern, ROWS + 32, smem, &per_sm);
   if (prc) return prc;
@@ -953,7 +979,9 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
     const u64 tiles = (nn + ROWS - 1) / ROWS;
     const u64 cap = (u64)sms * per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    kern<<<grid, ROWS + 32, smem, st>>>(map, proto, nn, len, out + base * W, tma_l2_prefetch());
+    kern<<<grid, ROWS + 32, smem, st>>>(map, proto, nn, len, STREAM ? out : out + base * W,
+                                        tma_l2_prefetch(), STREAM ? rec + base : nullptr,
+                                        msgs + base * len);
     int rc = cuda_err(cudaGetLastError());
     if (rc) return rc;
   }
@@ -1188,6 +1216,40 @@ static PrfProto prf_proto(const u64 key[4], int rounds) {
   p.h = h;
   return p;
 }
+
+namespace {
+template <class H>
+int launch_tma_stream(StreamRec<H>* rec, const uint8_t* chunks, u64 n, u64 len,
+                      cudaStream_t st) {
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  H proto;
+  memset(&proto, 0, sizeof proto);  // unused: every row starts from its record
+  if (n >= (u64)sms * 512 * 8)
+    return launch_tma_cfg<H, 512, 3, 1, true>(proto, chunks, n, len, nullptr, st, sms, rec);
+  return launch_tma_cfg<H, 128, 4, 3, true>(proto, chunks, n, len, nullptr, st, sms, rec);
+}
+
+}  // namespace
+
+namespace lh {
+int stream_update_tma(int alg, void* d_state, u64 n, const uint8_t* d_chunks, u64 chunk_len,
+                      void* stream) {
+  if (n < 1024 || chunk_len % 32 || !tma_ok(d_chunks, n, chunk_len)) return LH_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (alg) {
+    case LH_ALG_HIGHWAY:
+      return launch_tma_stream((StreamRec<Highway>*)d_state, d_chunks, n, chunk_len, st);
+    case LH_ALG_SIPHASH:
+      return launch_tma_stream((StreamRec<Sip<0, 0>>*)d_state, d_chunks, n, chunk_len, st);
+    case LH_ALG_SIPTREE:
+      return launch_tma_stream((StreamRec<SipTree<0, 0>>*)d_state, d_chunks, n, chunk_len, st);
+    default:
+      return LH_EINVAL;
+  }
+}
+}  // namespace lh
 
 // ==========================================================================
 // extern "C" boundary

@@ -20,19 +20,11 @@
 #include "lh_device.cuh"
 #include "lh_host.cuh"
 #include "lh_reader.cuh"
+#include "lh_stream.cuh"
 
 using namespace lh;
 
 namespace {
-
-template <class H>
-struct __align__(16) StreamRec {
-  H h;
-  u64 total;    // bytes appended so far
-  u64 tail[4];  // pending bytes (LE), zero past tlen
-  u32 tlen;     // 0..31
-  u32 pad;
-};
 
 template <class H>
 __global__ void k_stream_init(StreamRec<H>* __restrict__ rec, const H proto, u64 n) {
@@ -46,12 +38,6 @@ __global__ void k_stream_init(StreamRec<H>* __restrict__ rec, const H proto, u64
     r.pad = 0;
     rec[i] = r;
   }
-}
-
-__device__ __forceinline__ void put_byte(u64 (&t)[4], u32 pos, u32 byte) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if ((pos >> 3) == (u32)k) t[k] |= (u64)byte << (8 * (pos & 7));
 }
 
 template <class H>
@@ -72,24 +58,7 @@ __global__ void k_stream_update(StreamRec<H>* __restrict__ rec, u64 n,
     }
     if (len == 0) continue;
     StreamRec<H> r = rec[i];
-    u32 t = r.tlen;
-    r.total += len;
-    if (t + len < 32) {  // everything stays pending
-      for (u32 j = 0; j < (u32)len; ++j) put_byte(r.tail, t + j, p[j]);
-      r.tlen = t + (u32)len;
-    } else {
-      if (t) {  // complete the pending block from the chunk's first bytes
-        const u32 need = 32 - t;
-        for (u32 j = 0; j < need; ++j) put_byte(r.tail, t + j, p[j]);
-        r.h.absorb32(r.tail);
-        p += need;
-        len -= need;
-      }
-      absorb_blocks(r.h, p, len >> 5);
-      const u32 rem = (u32)(len & 31);
-      load_tail(p + (len & ~31ull), rem, r.tail);
-      r.tlen = rem;
-    }
+    stream_append(r, p, len);
     rec[i] = r;
   }
 }
@@ -168,6 +137,12 @@ int lh_stream_update(int alg, void* d_state, uint64_t n, const uint8_t* d_buf,
   if ((uintptr_t)d_state % 16 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
     return LH_EALIGN;
   if (!n) return LH_OK;
+  if (!d_offsets) {
+    // Whole-block fixed-layout chunks: TMA-staged rows (rows with a pending
+    // tail take the generic append inside that kernel).
+    const int rc = stream_update_tma(alg, d_state, n, d_buf, chunk_len, stream);
+    if (rc != LH_EINVAL) return rc;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned g = grid_for(n);
   switch (alg) {

@@ -7,6 +7,7 @@ the CPU oracle; misuse raises RuntimeError like the reference hashers.
 """
 import numpy as np
 import pytest
+import torch
 
 import paper_1612_06257_b200 as lh
 from paper_1612_06257_b200 import engine, synth
@@ -180,3 +181,38 @@ def test_stream_finalization_rounds(oracle, rounds):
     got = to_u64(sb.finish())
     assert np.array_equal(got, oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), data,
                                                   256, rounds))
+
+
+@pytest.mark.parametrize("alg", [ALG_HIGHWAY, ALG_SIPHASH, ALG_SIPTREE])
+def test_tma_block_appends_with_and_without_pending_tails(oracle, alg):
+    """Fixed-layout whole-block chunks on >= 1,024 messages take the
+    TMA-staged append; rows left with a pending tail by an earlier ragged
+    append take the generic path inside it.  Digests equal the one-shot."""
+    rng = np.random.default_rng(alg + 40)
+    n = 3000
+    chunks = [128, 96, 1024, 32]
+    key = synth.key256() if alg == ALG_HIGHWAY else synth.key128()
+    # Rows 0..n/2 get a ragged head of 0..40 bytes first (pending tails).
+    head = rng.integers(0, 41, n).astype(np.uint32)
+    head[n // 2:] = 0
+    total = head.astype(np.int64) + sum(chunks)
+    msgs = [synth.counter_bytes(500 + i, int(t)) for i, t in enumerate(total)]
+    sb = engine.StreamBatch(alg, key, n)
+    off = np.zeros(n, np.uint64)
+    off[1:] = np.cumsum(head[:-1])
+    hb = np.concatenate([m[:h] for m, h in zip(msgs, head)]) if head.sum() else np.zeros(1, np.uint8)
+    sb.append(hb, off, head)
+    pos = head.astype(np.int64).copy()
+    for c in chunks:
+        block = np.stack([m[p:p + c] for m, p in zip(msgs, pos)])
+        sb.append(torch.from_numpy(block).cuda())
+        pos += c
+    got = to_u64(sb.finish())
+    buf = np.concatenate(msgs)
+    moff = np.zeros(n + 1, np.uint64)
+    moff[1:] = np.cumsum(total)
+    oalg = {ALG_HIGHWAY: oracle.ALG_HIGHWAY, ALG_SIPHASH: oracle.ALG_SIPHASH,
+            ALG_SIPTREE: oracle.ALG_SIPTREE}[alg]
+    p1, p2 = (64, 4) if alg == ALG_HIGHWAY else (2, 4)
+    want = oracle.batch_ragged(oalg, key, buf, moff, None, p1, p2)
+    assert np.array_equal(got, want)
