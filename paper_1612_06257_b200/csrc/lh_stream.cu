@@ -58,7 +58,7 @@ __global__ void k_stream_update(StreamRec<H>* __restrict__ rec, u64 n,
     }
     if (len == 0) continue;
     StreamRec<H> r = rec[i];
-    stream_append(r, p, len);
+    stream_append<true>(r, p, len);
     rec[i] = r;
   }
 }

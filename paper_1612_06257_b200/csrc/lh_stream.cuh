@@ -26,8 +26,10 @@ __device__ __forceinline__ void put_byte(u64 (&t)[4], u32 pos, u32 byte) {
 
 // Append len bytes at p to one message's record (S/highway.py:257-285,
 // S/sip.py:131-203): complete a pending block, absorb whole blocks, keep
-// the rest pending.
-template <class H>
+// the rest pending.  RING: whole blocks through the branch-free register-ring
+// reader (the streaming kernel); otherwise the plain reader (the fallback
+// inside the TMA-staged append, where registers are scarce).
+template <bool RING, class H>
 __device__ __forceinline__ void stream_append(StreamRec<H>& r, const uint8_t* p, u64 len) {
   if (len == 0) return;
   const u32 t = r.tlen;
@@ -44,10 +46,15 @@ __device__ __forceinline__ void stream_append(StreamRec<H>& r, const uint8_t* p,
     p += need;
     len -= need;
   }
-  absorb_blocks(r.h, p, len >> 5);
-  const u32 rem = (u32)(len & 31);
-  load_tail(p + (len & ~31ull), rem, r.tail);
-  r.tlen = rem;
+  if constexpr (!RING) {
+    absorb_blocks(r.h, p, len >> 5);
+    load_tail(p + (len & ~31ull), (u32)(len & 31), r.tail);
+  } else if constexpr (RingWide<H>::value) {
+    absorb_ring64<2>(r.h, p, len, r.tail);  // 2 blocks in flight
+  } else {
+    absorb_ring<2>(r.h, p, len, r.tail);
+  }
+  r.tlen = (u32)(len & 31);
 }
 
 // TMA-staged append of fixed-layout chunks of chunk_len bytes (a multiple
