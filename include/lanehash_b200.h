@@ -52,7 +52,7 @@ extern "C" {
 #define LH_KERNEL_STAGED 4 /* HighwayHash: warp-staged short-key kernel
                               (ragged, or fixed rows) */
 #define LH_KERNEL_RING 5   /* one thread per message, branch-free word reader
-                              with 4 packets in flight (fixed or ragged) */
+                              with 2 packets in flight (fixed or ragged) */
 
 /* Library / build identification. */
 const char* lh_version(void);
@@ -84,7 +84,7 @@ int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets,
  * (messages <= 64 B packed together; any other warp reads its messages
  * directly);
  * LH_KERNEL_RING (or LH_KERNEL_DIRECT) = one thread per message with a
- * register ring of 4 packets in flight (medium/long messages, e.g. the
+ * register ring of 2 packets in flight (medium/long messages, e.g. the
  * L = 0..1023 sweep). */
 int lh_highway_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
                              const uint32_t* d_lengths, uint64_t n,

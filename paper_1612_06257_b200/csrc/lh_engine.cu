@@ -768,7 +768,7 @@ int launch_direct(const H& proto, const uint8_t* buf, const u64* offsets, const 
 // Register-ring reader for ragged batches of medium/long messages
 // (LH_KERNEL_DIRECT on the ragged entry points).
 #ifndef LH_RING_DEPTH
-#define LH_RING_DEPTH 4
+#define LH_RING_DEPTH 2
 #endif
 constexpr int kRingDepth = LH_RING_DEPTH;
 
