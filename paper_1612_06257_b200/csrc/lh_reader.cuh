@@ -232,6 +232,77 @@ __device__ __forceinline__ void absorb_ring64(H& h, const uint8_t* msg, u64 len,
   }
 }
 
+// The same reader over 16-byte words (2 loads per packet instead of 5 or
+// 9: per-lane loads of different messages are separate L1 sector requests,
+// which bound the small, latency-exposed ragged batches).  The 12 32-bit
+// words of three consecutive 16-byte loads feed the output words m =
+// funnel_r(U[m + o], U[m + o + 1], s) with o = (addr >> 2) & 3 selected by
+// two SEL levels and s = 8 * (addr & 3).
+template <int D, class H>
+__device__ __forceinline__ void absorb_ring128(H& h, const uint8_t* msg, u64 len, u64 (&t)[4]) {
+  const uintptr_t a = (uintptr_t)msg;
+  const uint4* w = (const uint4*)(a & ~(uintptr_t)15);
+  const u32 o = (u32)(a >> 2) & 3u, s = (u32)(a & 3) * 8;
+  const u64 nb = len >> 5;
+  const u32 r = (u32)(len & 31);
+  const u64 lastw = len ? ((a + len - 1) >> 4) - (a >> 4) : 0;  // last 16-B word with a message byte
+  auto ld = [&](u64 k) { return __ldg(w + (k < lastw ? k : lastw)); };
+  // Full packet pk covers 16-byte words 2pk .. 2pk+2; words up to 2pk+1
+  // always hold message bytes, only 2pk+2 is clamped.
+  auto ld_packet = [&](uint4 (&x)[2], u64 pk) {
+    const uint4* p = w + 2 * pk;
+    x[0] = __ldg(p + 1);
+    x[1] = __ldg(2 * pk + 2 < lastw ? p + 2 : w + lastw);
+  };
+  auto packet = [&](const uint4& f, const uint4 (&x)[2], u64 (&p)[4]) {
+    const u32 U[12] = {f.x, f.y, f.z, f.w, x[0].x, x[0].y, x[0].z, x[0].w,
+                       x[1].x, x[1].y, x[1].z, x[1].w};
+    u32 A[11], V[9];
+#pragma unroll
+    for (int j = 0; j < 11; ++j) A[j] = (o & 1u) ? U[j + 1] : U[j];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) V[j] = (o & 2u) ? A[j + 2] : A[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      p[j] = pack(__funnelshift_r(V[2 * j], V[2 * j + 1], s),
+                  __funnelshift_r(V[2 * j + 1], V[2 * j + 2], s));
+  };
+  uint4 ring[D][2];
+  uint4 first = len ? __ldg(w) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    if ((u64)k < nb) ld_packet(ring[k], (u64)k);
+  u64 b = 0;
+  for (; b + D <= nb; b += D) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      u64 p[4];
+      packet(first, ring[k], p);
+      first = ring[k][1];
+      if (b + k + D < nb) ld_packet(ring[k], b + k + D);
+      h.absorb32(p);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) {
+    if (b + k < nb) {
+      u64 p[4];
+      packet(first, ring[k], p);
+      first = ring[k][1];
+      h.absorb32(p);
+    }
+  }
+  t[0] = t[1] = t[2] = t[3] = 0;
+  if (r) {
+    uint4 x[2];
+    const u64 base = 2 * nb;
+    x[0] = ld(base + 1);
+    x[1] = ld(base + 2);
+    packet(first, x, t);
+    mask_tail(t, r);
+  }
+}
+
 // 8-byte words for HighwayHash (cfg2 26.6 -> 22.5 us; 4 GiB of 512..1536-B
 // messages 1.72 -> 1.33 ms); 4-byte words for the Sip family, whose extra
 // ALU work makes the 64-bit form's selects cost more than the loads it saves.
