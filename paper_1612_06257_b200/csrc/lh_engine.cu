@@ -785,6 +785,8 @@ int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u3
   // Word size (scripts/ragged_ab.py, untiled_ab.py): Sip 4 bytes; HighwayHash
   // 8 for ragged batches, 16 for fixed rows (2^18 x 4095 B: 0.428 -> 0.252 ms).
   const unsigned grid = grid_for(n, 128, sms);
+  // Ring depth: 2 for HighwayHash (equal or better than 4 everywhere), 4 for
+  // Sip (cfg3-shaped SipHash-2-4: 2.86 ms at depth 4, 3.09 at depth 2).
   if constexpr (std::is_same<H, Highway>::value) {
     if (!offsets)
       k_ragged_ring<H, kRingDepth, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
@@ -793,8 +795,8 @@ int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u3
       k_ragged_ring<H, kRingDepth, 8><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
                                                               fixed_len, n, out);
   } else {
-    k_ragged_ring<H, kRingDepth, 4><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
-                                                            fixed_len, n, out);
+    k_ragged_ring<H, 4, 4><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths, fixed_len, n,
+                                                   out);
   }
   return cuda_err(cudaGetLastError());
 }
