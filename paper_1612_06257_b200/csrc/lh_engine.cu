@@ -522,8 +522,8 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
 // (16 x 512 B = 8 KiB for CH = 4), laid out [chunk][row][128 B] with the
 // 128-byte swizzle, into a STAGES-deep ring refilled by lane 0 as soon as
 // the warp has consumed a stage.  Half 0 of row r reads unit 2k of packet
-// k, half 1 unit 2k+1 (2-way bank conflict; shared memory is not the
-// limiter here).
+// k, half 1 unit 2k+1; the lane -> row map keeps each quarter-warp's
+// units in distinct banks.
 // --------------------------------------------------------------------------
 constexpr int kSplitRows = 16;
 
@@ -541,7 +541,11 @@ __global__ void __launch_bounds__(32, MINB)
   constexpr u32 kChunk = kSplitRows * kBoxBytes;  // 2 KiB: one 128-B chunk of 16 rows
   constexpr u32 kStage = CH * kChunk;
   uint64_t* bar = (uint64_t*)(smem + STAGES * kStage);
-  const u32 lane = threadIdx.x & 31, row = lane >> 1, half = lane & 1, sw = row & 7;
+  // Lane -> row: each quarter-warp (8 lanes) takes rows whose swizzle
+  // patterns r & 7 differ in bits 1-2 (rows 0,2,4,6 / 1,3,5,7 / 8,10,.. /
+  // 9,11,..), so the 8 LDS.128 units it reads per packet are distinct banks.
+  const u32 lane = threadIdx.x & 31, half = lane & 1;
+  const u32 row = ((lane >> 1) & 3) * 2 + ((lane >> 3) & 1) + (lane >> 4) * 8, sw = row & 7;
 
   const u64 ntiles = (n + kSplitRows - 1) / kSplitRows;
   const u32 nch = (u32)(len / kBoxBytes);
