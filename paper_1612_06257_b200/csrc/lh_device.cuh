@@ -300,6 +300,17 @@ struct HighwayHalf {
     }
   }
 
+  // Writes this half's two lanes back into a full state (streaming).
+  __device__ __forceinline__ void save(Highway& full) const {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      full.v0[2 * half + i] = v0[i];
+      full.v1[2 * half + i] = v1[i];
+      full.m0[2 * half + i] = m0[i];
+      full.m1[2 * half + i] = m1[i];
+    }
+  }
+
   // Writes this half's lanes of the width/64 lane sums (lane 0 first).
   __device__ __forceinline__ void store(u64* out) const {
     const u64 s0 = v0[0] + v1[0] + m0[0] + m1[0];

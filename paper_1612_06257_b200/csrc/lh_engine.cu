@@ -532,10 +532,15 @@ constexpr size_t split_smem_bytes() {
   return 1024 + (size_t)STAGES * kSplitRows * CH * kBoxBytes + STAGES * 8;
 }
 
-template <int STAGES, int CH, int MINB>
+// STREAM: the streaming append of whole-block chunks (as k_tma_fixed's):
+// each half starts from its lanes of the message's StreamRec state and
+// writes them back; a row with a pending tail skips the staged data and its
+// half 0 runs the generic append from global memory.
+template <int STAGES, int CH, int MINB, bool STREAM = false>
 __global__ void __launch_bounds__(32, MINB)
     k_tma_split(const __grid_constant__ CUtensorMap tmap, const Highway proto, u64 n, u64 len,
-                u64* __restrict__ out) {
+                u64* __restrict__ out, StreamRec<Highway>* __restrict__ rec = nullptr,
+                const uint8_t* __restrict__ chunks = nullptr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr u32 kChunk = kSplitRows * kBoxBytes;  // 2 KiB: one 128-B chunk of 16 rows
@@ -584,8 +589,24 @@ __global__ void __launch_bounds__(32, MINB)
 
   const int W = proto.width / 64;
   HighwayHalf h;
-  h.init(proto, half);
+  bool fast = true;
+  // Row state at the start of a tile: the prototype, or (STREAM) the record.
+  auto start_row = [&](u64 tl) {
+    const u64 m = tl * kSplitRows + row;
+    if constexpr (STREAM) {
+      fast = true;
+      if (m < n) {
+        h.init(rec[m].h, half);
+        fast = rec[m].tlen == 0;
+      } else {
+        h.init(proto, half);
+      }
+    } else {
+      h.init(proto, half);
+    }
+  };
   u64 tile = g;
+  start_row(tile);
   u32 st = 0, s = 0, ph = 0;
   for (u64 i = 0; i < total; ++i) {
     mbar_wait(&bar[s], ph);
@@ -599,7 +620,7 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll
             for (u32 k = 0; k < 4; ++k) {
               const uint4 a = lds128(ua[k] + ss * kStage + c * kChunk);
-              h.update(pack(a.x, a.y), pack(a.z, a.w));
+              if (!STREAM || fast) h.update(pack(a.x, a.y), pack(a.z, a.w));
             }
         }
       }
@@ -608,7 +629,7 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll
         for (u32 k = 0; k < 4; ++k) {
           const uint4 a = lds128(ua[k] + s * kStage + c * kChunk);
-          h.update(pack(a.x, a.y), pack(a.z, a.w));
+          if (!STREAM || fast) h.update(pack(a.x, a.y), pack(a.z, a.w));
         }
     }
     __syncwarp();
@@ -621,12 +642,25 @@ __global__ void __launch_bounds__(32, MINB)
       ph ^= 1;
     }
     if (++st == nst) {
-      h.finalize_rounds();  // whole warp: shuffles between the halves
       const u64 m = tile * kSplitRows + row;
-      if (m < n) h.store(out + m * W);
-      h.init(proto, half);
+      if constexpr (STREAM) {
+        if (m < n) {
+          if (fast) {
+            h.save(rec[m].h);
+            if (half == 0) rec[m].total += len;
+          } else if (half == 0) {
+            StreamRec<Highway> rr = rec[m];
+            stream_append<false>(rr, chunks + m * len, len);
+            rec[m] = rr;
+          }
+        }
+      } else {
+        h.finalize_rounds();  // whole warp: shuffles between the halves
+        if (m < n) h.store(out + m * W);
+      }
       st = 0;
       tile += G;
+      start_row(tile);
     }
   }
 }
@@ -858,8 +892,9 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
   return LH_OK;
 }
 
+template <bool STREAM = false>
 int launch_split(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
-                 cudaStream_t st) {
+                 cudaStream_t st, StreamRec<Highway>* rec = nullptr) {
   constexpr int STAGES = 3, CH = 4, MINB = 8;
   int sms = 0;
   int rc = check_device(&sms);
@@ -868,7 +903,7 @@ int launch_split(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64*
   auto enc = get_encode();
   if (!enc) return LH_ECUDA;
   constexpr size_t smem = split_smem_bytes<STAGES, CH>();
-  auto kern = k_tma_split<STAGES, CH, MINB>;
+  auto kern = k_tma_split<STAGES, CH, MINB, STREAM>;
   int per_sm = 0;
   rc = prepare_kernel((const void*)kern, 32, smem, &per_sm);
   if (rc) return rc;
@@ -889,7 +924,8 @@ int launch_split(const Highway& proto, const uint8_t* msgs, u64 n, u64 len, u64*
     const u64 tiles = (nn + kSplitRows - 1) / kSplitRows;
     const u64 cap = (u64)sms * per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    kern<<<grid, 32, smem, st>>>(map, proto, nn, len, out + base * W);
+    kern<<<grid, 32, smem, st>>>(map, proto, nn, len, STREAM ? out : out + base * W,
+                                 STREAM ? rec + base : nullptr, msgs + base * len);
     rc = cuda_err(cudaGetLastError());
     if (rc) return rc;
   }
@@ -1109,8 +1145,14 @@ int stream_update_tma(int alg, void* d_state, u64 n, const uint8_t* d_chunks, u6
   if (n < 1024 || chunk_len % 32 || !tma_ok(d_chunks, n, chunk_len)) return LH_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   switch (alg) {
-    case LH_ALG_HIGHWAY:
+    case LH_ALG_HIGHWAY: {
+      Highway proto;
+      memset(&proto, 0, sizeof proto);
+      if (prefer_split(proto, d_chunks, n, chunk_len))  // few long chunks: 2 threads per row
+        return launch_split<true>(proto, d_chunks, n, chunk_len, nullptr, st,
+                                  (StreamRec<Highway>*)d_state);
       return launch_tma_stream((StreamRec<Highway>*)d_state, d_chunks, n, chunk_len, st);
+    }
     case LH_ALG_SIPHASH:
       return launch_tma_stream((StreamRec<Sip<0, 0>>*)d_state, d_chunks, n, chunk_len, st);
     case LH_ALG_SIPTREE:
