@@ -197,6 +197,28 @@ def _launch_fixed(kind, key, d_msgs: torch.Tensor, n: int, L: int, p1: int, p2: 
 
 
 def _fixed(kind, key, msgs, p1, p2, tree, lanes, kernel, out=None):
+    # Fast path for the common small-batch call (a contiguous uint8 CUDA
+    # tensor on the current device): one ctypes call, no device switch.
+    if (isinstance(msgs, torch.Tensor) and msgs.is_cuda and msgs.dtype is torch.uint8
+            and msgs.dim() == 2 and msgs.is_contiguous()):
+        idx = msgs.get_device()
+        if _CUDA_CHECKED and idx == torch.cuda.current_device():
+            n, L = msgs.shape
+            if out is None:
+                out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=msgs.device)
+            if n:
+                st = _raw_stream(idx) if _raw_stream is not None else \
+                    torch.cuda.current_stream(idx).cuda_stream
+                ptr = msgs.data_ptr() if L else 0
+                if kind == "hh":
+                    rc = _lib.lib().lh_highway_fixed_kernel(ptr, n, L, _key4(key), p1, p2,
+                                                            out.data_ptr(), st, kernel)
+                else:
+                    rc = _lib.lib().lh_siphash_fixed_kernel(ptr, n, L, _key2(key), p1, p2, tree,
+                                                            out.data_ptr(), st, kernel)
+                if rc:
+                    _lib.check(rc, "lh_highway_fixed" if kind == "hh" else "lh_siphash_fixed")
+            return out
     device = _require_cuda()
     m = _as_u8_2d(msgs)
     n, L = m.shape

@@ -64,6 +64,11 @@ def main():
         "cfg1 engine.highway_batch": lambda: engine.highway_batch(key, msgs, 64, out=o),
         "cfg1 raw ctypes lh_highway_fixed": lambda: lib.lh_highway_fixed(
             msgs.data_ptr(), 4096, 1024, k4, 64, 4, o.data_ptr(), st),
+        "cfg1 raw ctypes, n = 0 (argument checks only)": lambda: lib.lh_highway_fixed(
+            msgs.data_ptr(), 0, 1024, k4, 64, 4, o.data_ptr(), st),
+        "cfg1 raw ctypes, direct kernel (no tensor map)": lambda: lib.lh_highway_fixed_kernel(
+            msgs.data_ptr(), 4096, 1024, k4, 64, 4, o.data_ptr(), st, engine.KERNEL_DIRECT),
+        "lh_version (bare ctypes call)": lambda: lib.lh_version(),
         "cfg2 engine.highway_ragged": lambda: engine.highway_ragged(key, d_b, d_off, None, 64,
                                                                     out=o2),
         "cfg2 raw ctypes lh_highway_ragged_kernel(ring)": lambda: lib.lh_highway_ragged_kernel(
