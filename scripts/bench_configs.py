@@ -176,6 +176,15 @@ def main():
         ms, _ = time_launch(lambda: engine.highway_batch(key, msgs, 64, out=o), a.steps, a.warmup)
         emit(row("cfg1 4096 x 1 KiB hh64", ms, 4096 * 1024, 4096, 4096 * 1032,
                  "L2-resident, launch-bound"))
+        # The same call captured 32 times in a CUDA graph: the host launch
+        # cost (~9 us per Python call) leaves; the kernel's own time remains.
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(32):
+                engine.highway_batch(key, msgs, 64, out=o)
+        ms, _ = time_launch(g.replay, max(3, a.steps // 4), 2)
+        emit(row("cfg1 4096 x 1 KiB hh64, CUDA-graph replay (per call)", ms / 32, 4096 * 1024,
+                 4096, 4096 * 1032, "kernel-bound: 36-Update chain per thread pair"))
 
     if on("e2e"):
         # End to end from pinned host memory through the public API (H2D, kernel, D2H).
