@@ -187,13 +187,9 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
 // The ring readers (lh_reader.cuh) with WORD-byte loads, then finalization.
 template <int D, int WORD, class H>
 __device__ __forceinline__ void hash_ring_any(H& h, const uint8_t* msg, u64 len, u64* out) {
+  static_assert(WORD == 16, "the ring reader loads 16-byte words");
   u64 t[4];
-  if constexpr (WORD == 16)
-    absorb_ring128<D>(h, msg, len, t);
-  else if constexpr (WORD == 8)
-    absorb_ring64<D>(h, msg, len, t);
-  else
-    absorb_ring<D>(h, msg, len, t);
+  absorb_ring128<D>(h, msg, len, t);
   h.finish(t, (u32)(len & 31), len, out);
 }
 
@@ -820,22 +816,18 @@ int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u3
   int rc = check_device(&sms);
   if (rc) return rc;
   if (n == 0) return LH_OK;
-  // Word size (scripts/ragged_ab.py, untiled_ab.py): Sip 4 bytes; HighwayHash
-  // 8 for ragged batches, 16 for fixed rows (2^18 x 4095 B: 0.428 -> 0.252 ms).
-  const unsigned grid = grid_for(n, 128, sms);
+  // 16-byte word loads for every hash (scripts/ring_word_ab.py): 4- and
+  // 8-byte per-lane loads of messages a power-of-two apart (256 B, 4 KiB
+  // records) ran 2-3.5x slower; 16-byte loads cost 1-6% on random lengths.
   // Ring depth: 2 for HighwayHash (equal or better than 4 everywhere), 4 for
-  // Sip (cfg3-shaped SipHash-2-4: 2.86 ms at depth 4, 3.09 at depth 2).
-  if constexpr (std::is_same<H, Highway>::value) {
-    if (!offsets)
-      k_ragged_ring<H, kRingDepth, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
-                                                               fixed_len, n, out);
-    else
-      k_ragged_ring<H, kRingDepth, 8><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
-                                                              fixed_len, n, out);
-  } else {
-    k_ragged_ring<H, 4, 4><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths, fixed_len, n,
-                                                   out);
-  }
+  // Sip (short keys need it: cfg3-shaped SipHash-2-4 2.85 ms vs 3.09).
+  const unsigned grid = grid_for(n, 128, sms);
+  if constexpr (std::is_same<H, Highway>::value)
+    k_ragged_ring<H, kRingDepth, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
+                                                             fixed_len, n, out);
+  else
+    k_ragged_ring<H, 4, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths, fixed_len, n,
+                                                    out);
   return cuda_err(cudaGetLastError());
 }
 
