@@ -1035,6 +1035,19 @@ int dispatch_untiled<Highway>(const Highway& proto, const uint8_t* msgs, u64 n, 
   return launch_direct(proto, msgs, nullptr, nullptr, len, n, out, st);
 }
 
+// SipHash (not SipTree) rows of 32..127 bytes: the register-ring
+// kernel beats the TMA ring by 8-25% (scripts/untiled_ab.py-style sweep,
+// SipHash-1-3 at 64 B 0.414 vs 0.522 ms per GiB); from 128 B,
+// and for SipTree at every length, the TMA kernel is faster.
+template <class H>
+struct ShortRowsToRing {
+  static constexpr bool value = false;
+};
+template <int C, int D>
+struct ShortRowsToRing<Sip<C, D>> {
+  static constexpr bool value = true;
+};
+
 template <class H>
 int dispatch_fixed(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                    cudaStream_t st, int kernel) {
@@ -1047,6 +1060,9 @@ int dispatch_fixed(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
   }
   if (kernel == LH_KERNEL_RING) return launch_ring(proto, msgs, nullptr, nullptr, len, n, out, st);
   if (kernel == LH_KERNEL_STAGED) return dispatch_staged(proto, msgs, n, len, out, st);
+  if (kernel == LH_KERNEL_AUTO && ShortRowsToRing<H>::value && len >= 32 && len < 128 &&
+      n >= 1024)
+    return launch_ring(proto, msgs, nullptr, nullptr, len, n, out, st);
   if (kernel == LH_KERNEL_AUTO && tma_ok(msgs, n, len) && n >= 1024)
     return launch_tma(proto, msgs, n, len, out, st);
   if (kernel == LH_KERNEL_AUTO) return dispatch_untiled(proto, msgs, n, len, out, st);
