@@ -51,8 +51,9 @@ extern "C" {
                               message (long messages; len % 128 == 0) */
 #define LH_KERNEL_STAGED 4 /* HighwayHash: warp-staged short-key kernel
                               (ragged, or fixed rows) */
-#define LH_KERNEL_RING 5   /* one thread per message, branch-free word reader
-                              with 2 packets in flight (fixed or ragged) */
+#define LH_KERNEL_RING 5   /* one thread per message, branch-free 16-byte
+                              word reader with packets in flight (fixed or
+                              ragged) */
 
 /* Library / build identification. */
 const char* lh_version(void);
@@ -66,6 +67,9 @@ const char* lh_strerror(int code);
 int lh_highway_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len,
                      const uint64_t key[4], int width, int rounds,
                      uint64_t* d_out, void* stream);
+/* kernel: any LH_KERNEL_*.  AUTO: TMA for rows that are 16-byte multiples
+ * (>= 1,024 rows), SPLIT for few long rows, STAGED for rows <= 64 B and
+ * RING for longer rows that TMA cannot take. */
 int lh_highway_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
                             const uint64_t key[4], int width, int rounds,
                             uint64_t* d_out, void* stream, int kernel);
@@ -84,7 +88,7 @@ int lh_highway_ragged(const uint8_t* d_buf, const uint64_t* d_offsets,
  * (messages <= 64 B packed together; any other warp reads its messages
  * directly);
  * LH_KERNEL_RING (or LH_KERNEL_DIRECT) = one thread per message with a
- * register ring of 2 packets in flight (medium/long messages, e.g. the
+ * register ring of packets in flight (medium/long messages, e.g. the
  * L = 0..1023 sweep). */
 int lh_highway_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
                              const uint32_t* d_lengths, uint64_t n,
@@ -97,6 +101,8 @@ int lh_highway_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
 int lh_siphash_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len,
                      const uint64_t key[2], int c, int d, int tree,
                      uint64_t* d_out, void* stream);
+/* kernel: LH_KERNEL_AUTO, LH_KERNEL_DIRECT, LH_KERNEL_TMA or LH_KERNEL_RING
+ * (SPLIT and STAGED are HighwayHash only). */
 int lh_siphash_fixed_kernel(const uint8_t* d_msgs, uint64_t n, uint64_t len,
                             const uint64_t key[2], int c, int d, int tree,
                             uint64_t* d_out, void* stream, int kernel);
