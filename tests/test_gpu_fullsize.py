@@ -158,3 +158,25 @@ def test_tuning_tile_shapes_are_bit_exact(cfg):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("kernel,L", [(KERNEL_TMA, 32), (KERNEL_SPLIT, 128)])
+def test_row_segments_past_2p30(oracle, kernel, L):
+    """More than 2^30 rows: the TMA and split kernels take the batch in
+    segments of 2^30 rows (TMA coordinates are int32).  Rows on both sides
+    of every segment boundary and a random sample match the oracle."""
+    n = (1 << 30) + 4096 if kernel == KERNEL_TMA else (1 << 30) + 200
+    if torch.cuda.get_device_properties(0).total_memory < n * (L + 8) * 1.2:
+        pytest.skip("needs more device memory")
+    buf = _fill(n * L, 17)
+    m = buf.view(n, L)
+    out = engine.highway_batch(synth.key256(), m, 64, kernel=kernel)
+    rng = np.random.default_rng(3)
+    idx = np.unique(np.concatenate([[0, (1 << 30) - 1, 1 << 30, (1 << 30) + 1, n - 1],
+                                    rng.integers(0, n, 200)]))
+    got = to_u64(out[torch.from_numpy(idx).to(DEV)])
+    rows = m[torch.from_numpy(idx).to(DEV)].cpu().numpy()
+    want = oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), rows, 64, 4)
+    assert np.array_equal(got, want)
+    del buf, m, out
+    torch.cuda.empty_cache()
