@@ -180,3 +180,30 @@ def test_row_segments_past_2p30(oracle, kernel, L):
     assert np.array_equal(got, want)
     del buf, m, out
     torch.cuda.empty_cache()
+
+
+def test_ragged_offsets_past_4gib(oracle):
+    """Byte offsets beyond 2^32 (u64 offset arithmetic in every ragged
+    kernel): messages straddling and past the 4 GiB mark."""
+    from paper_1612_06257_b200.engine import KERNEL_RING, KERNEL_STAGED
+    total = (1 << 32) + (1 << 24)
+    buf = _fill(total, 23)
+    rng = np.random.default_rng(8)
+    lens = rng.integers(0, 700, 3000).astype(np.uint32)
+    lens[:1500] = rng.integers(0, 65, 1500)  # short keys for the staged kernel
+    off = np.zeros(3000, np.uint64)
+    off[1:] = np.cumsum(lens[:-1], dtype=np.uint64)
+    off += np.uint64((1 << 32) - 40000)  # the batch straddles the 4 GiB mark
+    span = buf[int(off[0]):int(off[-1]) + int(lens[-1])].cpu().numpy()
+    rel = off - off[0]
+    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), span, rel, lens, 64, 4)
+    d_off = torch.from_numpy(off.view(np.int64)).to(DEV)
+    d_len = torch.from_numpy(lens.view(np.int32)).to(DEV)
+    for kernel in (KERNEL_STAGED, KERNEL_RING):
+        got = to_u64(engine.highway_ragged(synth.key256(), buf, d_off, d_len, 64, kernel=kernel))
+        assert np.array_equal(got, want), kernel
+    got = to_u64(engine.sip_ragged(synth.key128(), buf, d_off, d_len, 2, 4))
+    assert np.array_equal(got, oracle.batch_ragged(oracle.ALG_SIPHASH, synth.key128(), span, rel,
+                                                   lens, 2, 4))
+    del buf
+    torch.cuda.empty_cache()
