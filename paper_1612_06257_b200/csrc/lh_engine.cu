@@ -2,22 +2,24 @@
 // (include/lanehash_b200.h).
 //
 // Kernels:
-//   k_tma_fixed<H,ROWS,STAGES>  fixed-length batch; one thread per message;
-//       a producer warp streams ROWS x 128-byte boxes of the (n, len) byte
-//       matrix into a STAGES-deep shared-memory ring with 2-D TMA
+//   k_tma_fixed<H,ROWS,STAGES[,STREAM]>  fixed-length batch; one thread per
+//       message; a producer warp streams ROWS x 128-byte boxes of the (n, len)
+//       byte matrix into a STAGES-deep shared-memory ring with 2-D TMA
 //       (SWIZZLE_128B, so each thread's 16-byte reads of its own row are
 //       bank-conflict free); consumer threads run the hash on registers.
+//       STREAM: the streaming append of whole-block chunks.
 //   k_tma_split  HighwayHash of few long messages: the state split over a
-//       thread pair, 3-D TMA boxes of 16 rows x 512 B per warp.
-//   k_ragged_short  ragged batches of short keys: warp-staged byte spans,
-//       non-divergent Update slots; falls back to the direct reader.
-//   k_ragged_ring<H,D>  ragged batches of medium/long messages (HighwayHash)
-//       and every ragged Sip batch: one thread per message, word reads
-//       branch-free in the alignment (8-byte words for HighwayHash, 4-byte
-//       for Sip), D packets in flight.
+//       thread pair, 3-D TMA boxes of 16 rows x 512 B per warp (also STREAM).
+//   k_ragged_short  short keys (ragged, or fixed rows <= 64 B): warp-staged
+//       byte spans, non-divergent Update slots; falls back to the direct
+//       reader.
+//   k_ragged_ring<H,D,16>  ragged batches of medium/long messages
+//       (HighwayHash), every ragged Sip batch and fixed rows TMA does not
+//       take: one thread per message, 16-byte word reads branch-free in the
+//       alignment (lh_reader.cuh: absorb_ring128), D packets in flight.
 //   k_direct<H>  any layout (fixed or ragged, any alignment/length); one
 //       thread per message reading its bytes with 8-byte-aligned loads and
-//       funnel shifts.
+//       funnel shifts (small batches; LH_KERNEL_DIRECT).
 //   k_prf        HighwayHash-64 of 8-byte LE counters (no input bytes).
 // H is one of lh::Highway, lh::Sip<C,D>, lh::SipTree<C,D> (lh_device.cuh).
 //
