@@ -244,49 +244,69 @@ __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
   }
 }
 
-template <int WARPS>
+#ifndef LH_SHORT_MPL
+#define LH_SHORT_MPL 4
+#endif
+// MPL messages per lane per warp iteration (a group of 32 * MPL consecutive
+// messages staged together, hashed one after another by each lane).
+template <int WARPS, int MPL = LH_SHORT_MPL>
 __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto,
                                                              const uint8_t* __restrict__ buf,
                                                              const u64* __restrict__ offsets,
                                                              const u32* __restrict__ lengths,
                                                              u64 fixed_len, u64 n,
                                                              u64* __restrict__ out) {
-  __shared__ __align__(16) uint4 stage[WARPS][kSpanCap / 16 + 8];
+  constexpr u32 kSpan = kSpanCap * MPL;
+  __shared__ __align__(16) uint4 stage[WARPS][kSpan / 16 + 8];
   const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = proto.width / 64;
   const u32* S = reinterpret_cast<const u32*>(&stage[warp][0]);
-  for (u64 base = ((u64)blockIdx.x * WARPS + warp) * 32; base < n;
-       base += (u64)gridDim.x * WARPS * 32) {
-    const u64 i = base + lane;
-    const bool valid = i < n;
-    u64 start = 0, len = 0;
-    if (valid) {
-      if (offsets) {
-        start = offsets[i];
-        len = lengths ? (u64)lengths[i] : offsets[i + 1] - start;
-      } else {  // fixed layout: message i = buf[i*L : (i+1)*L]
-        start = i * fixed_len;
-        len = fixed_len;
+  for (u64 base = ((u64)blockIdx.x * WARPS + warp) * 32 * MPL; base < n;
+       base += (u64)gridDim.x * WARPS * 32 * MPL) {
+    u64 start[MPL], len[MPL];
+#pragma unroll
+    for (int m = 0; m < MPL; ++m) {
+      const u64 i = base + 32 * m + lane;
+      start[m] = 0;
+      len[m] = 0;
+      if (i < n) {
+        if (offsets) {
+          start[m] = offsets[i];
+          len[m] = lengths ? (u64)lengths[i] : offsets[i + 1] - start[m];
+        } else {  // fixed layout: message i = buf[i*L : (i+1)*L]
+          start[m] = i * fixed_len;
+          len[m] = fixed_len;
+        }
       }
     }
     // Fast-path test with 32-bit warp reductions: every message lies in the
-    // window [s0, s0 + kSpanCap) that starts at lane 0's message (lane 0 is
-    // always valid) and is at most 64 bytes.  Packed batches always pass.
-    const u64 s0 = __shfl_sync(0xffffffffu, start, 0);
-    const bool fits = !valid || (len <= 64 && start >= s0 && start + len - s0 <= kSpanCap);
+    // window [s0, s0 + kSpan) that starts at the group's first message
+    // (always valid) and is at most 64 bytes.  Packed batches always pass.
+    const u64 s0 = __shfl_sync(0xffffffffu, start[0], 0);
+    bool fits = true;
+    u32 reach = 0;
+#pragma unroll
+    for (int m = 0; m < MPL; ++m) {
+      const bool valid = base + 32 * m + lane < n;
+      fits &= !valid || (len[m] <= 64 && start[m] >= s0 && start[m] + len[m] - s0 <= kSpan);
+      if (valid) reach = max(reach, (u32)(start[m] + len[m] - s0));
+    }
     if (__all_sync(0xffffffffu, fits)) {
-      const u32 span = __reduce_max_sync(0xffffffffu, valid ? (u32)(start + len - s0) : 0u);
+      const u32 span = __reduce_max_sync(0xffffffffu, reach);
       const u64 lo = s0, hi = s0 + span;
       // Align on the absolute address: d_buf itself need not be 16-B aligned.
-      const u64 base = (u64)(uintptr_t)buf;
-      const u64 lo_al = ((base + lo) & ~15ull) - base, hi_al = ((base + hi + 15) & ~15ull) - base;
+      const u64 bb = (u64)(uintptr_t)buf;
+      const u64 lo_al = ((bb + lo) & ~15ull) - bb, hi_al = ((bb + hi + 15) & ~15ull) - bb;
       const u32 nch = (u32)((hi_al - lo_al) >> 4);
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
       for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
       __syncwarp();
-      if (valid) {
-        const u32 o = (u32)(start - lo_al), a = o >> 2, sh = (o & 3) * 8;
-        const u32 L = (u32)len;
+#pragma unroll 1
+      for (int m = 0; m < MPL; ++m) {
+        const u64 i = base + 32 * m + lane;
+        if (i >= n) break;
+        const u32 o = (u32)(start[m] - lo_al), a = o >> 2, sh = (o & 3) * 8;
+        const u32 L = (u32)len[m];
         const u32 nfull = L >> 5, r = L & 31;
         // Word k of the message (LE; bytes past L belong to other messages).
         auto word = [&](u32 k) { return __funnelshift_r(S[a + k], S[a + k + 1], sh); };
@@ -318,9 +338,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
         h.finalize_out(out + i * W);
       }
       __syncwarp();
-    } else if (valid) {
-      Highway h = proto;
-      hash_direct<true>(h, buf + start, len, out + i * W);
+    } else {
+#pragma unroll 1
+      for (int m = 0; m < MPL; ++m) {
+        const u64 i = base + 32 * m + lane;
+        if (i < n) {
+          Highway h = proto;
+          hash_direct<true>(h, buf + start[m], len[m], out + i * W);
+        }
+      }
     }
   }
 }
@@ -840,8 +866,10 @@ int launch_staged(const Highway& proto, const uint8_t* buf, const u64* offsets,
   int rc = check_device(&sms);
   if (rc) return rc;
   if (n == 0) return LH_OK;
-  constexpr int kWarps = 4;  // 4 warps per block: 1% over 8, 16 (cfg3 1.908 vs 1.928 ms)
-  const u64 warps = (n + 31) / 32;
+  // 2 warps per block of 4 messages per lane (cfg3: MPL 1 / 4 warps 1.900 ms,
+  // MPL 2 1.859, MPL 4 1.805, MPL 4 / 2 warps 1.784, MPL 8 2.17).
+  constexpr int kWarps = 2;
+  const u64 warps = (n + 32 * LH_SHORT_MPL - 1) / (32 * LH_SHORT_MPL);
   const u64 cap = (u64)sms * 8 * (64 / kWarps);
   const u64 blocks = (warps + kWarps - 1) / kWarps;
   k_ragged_short<kWarps><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0, st>>>(
