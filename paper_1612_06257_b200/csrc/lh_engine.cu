@@ -352,6 +352,97 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
 }
 
 // --------------------------------------------------------------------------
+// The same warp staging for any hasher (the Sip family's short keys): the
+// window of 32 * MPL messages <= 64 B is staged once, then each lane hashes
+// its MPL messages one after another, reading 32-bit words from the stage
+// (absorb32 per whole block, the masked tail to finish).  Hashing several
+// keys per lane also evens out the per-lane work: SipHash's cost grows with
+// every 8-byte word, so lanes of one key each wait for the warp's longest.
+// --------------------------------------------------------------------------
+template <class H, int WARPS, int MPL>
+__global__ void __launch_bounds__(WARPS * 32) k_staged_any(const H proto,
+                                                           const uint8_t* __restrict__ buf,
+                                                           const u64* __restrict__ offsets,
+                                                           const u32* __restrict__ lengths,
+                                                           u64 fixed_len, u64 n,
+                                                           u64* __restrict__ out) {
+  constexpr u32 kSpan = kSpanCap * MPL;
+  __shared__ __align__(16) uint4 stage[WARPS][kSpan / 16 + 8];
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u32* S = reinterpret_cast<const u32*>(&stage[warp][0]);
+  for (u64 base = ((u64)blockIdx.x * WARPS + warp) * 32 * MPL; base < n;
+       base += (u64)gridDim.x * WARPS * 32 * MPL) {
+    u64 start[MPL], len[MPL];
+#pragma unroll
+    for (int m = 0; m < MPL; ++m) {
+      const u64 i = base + 32 * m + lane;
+      start[m] = 0;
+      len[m] = 0;
+      if (i < n) {
+        if (offsets) {
+          start[m] = offsets[i];
+          len[m] = lengths ? (u64)lengths[i] : offsets[i + 1] - start[m];
+        } else {
+          start[m] = i * fixed_len;
+          len[m] = fixed_len;
+        }
+      }
+    }
+    const u64 s0 = __shfl_sync(0xffffffffu, start[0], 0);
+    bool fits = true;
+    u32 reach = 0;
+#pragma unroll
+    for (int m = 0; m < MPL; ++m) {
+      const bool valid = base + 32 * m + lane < n;
+      fits &= !valid || (len[m] <= 64 && start[m] >= s0 && start[m] + len[m] - s0 <= kSpan);
+      if (valid) reach = max(reach, (u32)(start[m] + len[m] - s0));
+    }
+    if (__all_sync(0xffffffffu, fits)) {
+      const u32 span = __reduce_max_sync(0xffffffffu, reach);
+      const u64 bb = (u64)(uintptr_t)buf;
+      const u64 lo_al = ((bb + s0) & ~15ull) - bb, hi_al = ((bb + s0 + span + 15) & ~15ull) - bb;
+      const u32 nch = (u32)((hi_al - lo_al) >> 4);
+      const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
+      for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
+      __syncwarp();
+#pragma unroll 1
+      for (int m = 0; m < MPL; ++m) {
+        const u64 i = base + 32 * m + lane;
+        if (i >= n) break;
+        const u32 o = (u32)(start[m] - lo_al), a = o >> 2, sh = (o & 3) * 8;
+        const u32 L = (u32)len[m];
+        auto word = [&](u32 k) { return __funnelshift_r(S[a + k], S[a + k + 1], sh); };
+        H h = proto;
+        const u32 nb = L >> 5, r = L & 31;
+        for (u32 b = 0; b < nb; ++b) {
+          const u64 p[4] = {pack(word(8 * b), word(8 * b + 1)), pack(word(8 * b + 2), word(8 * b + 3)),
+                            pack(word(8 * b + 4), word(8 * b + 5)),
+                            pack(word(8 * b + 6), word(8 * b + 7))};
+          h.absorb32(p);
+        }
+        u64 t[4] = {0, 0, 0, 0};
+        if (r) {
+#pragma unroll
+          for (u32 k = 0; k < 4; ++k) t[k] = pack(word(8 * nb + 2 * k), word(8 * nb + 2 * k + 1));
+          mask_tail(t, r);
+        }
+        h.finish(t, r, L, out + i);
+      }
+      __syncwarp();
+    } else {
+#pragma unroll 1
+      for (int m = 0; m < MPL; ++m) {
+        const u64 i = base + 32 * m + lane;
+        if (i < n) {
+          H h = proto;
+          hash_direct<true>(h, buf + start[m], len[m], out + i);
+        }
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // TMA-staged fixed-length kernel.
 // Requirements (checked on the host): len % 16 == 0, d_msgs 16-B aligned.
 // Shared ring: STAGES x [ROWS rows x 128 B] with the 128-byte swizzle:
@@ -877,6 +968,26 @@ int launch_staged(const Highway& proto, const uint8_t* buf, const u64* offsets,
   return cuda_err(cudaGetLastError());
 }
 
+#ifndef LH_ANY_MPL
+#define LH_ANY_MPL 4
+#endif
+// Warp-staged short keys for the Sip family (one digest word per message).
+template <class H>
+int launch_staged_any(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths,
+                      u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
+  int sms = 0;
+  int rc = check_device(&sms);
+  if (rc) return rc;
+  if (n == 0) return LH_OK;
+  constexpr int kWarps = 2, kMpl = LH_ANY_MPL;
+  const u64 warps = (n + 32 * kMpl - 1) / (32 * kMpl);
+  const u64 cap = (u64)sms * 256;
+  const u64 blocks = (warps + kWarps - 1) / kWarps;
+  k_staged_any<H, kWarps, kMpl><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0, st>>>(
+      proto, buf, offsets, lengths, fixed_len, n, out);
+  return cuda_err(cudaGetLastError());
+}
+
 template <class H, int ROWS, int STAGES, int MINB, bool STREAM = false>
 int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                    cudaStream_t st, int sms, StreamRec<H>* rec = nullptr) {
@@ -1103,7 +1214,8 @@ bool valid_width(int w) { return w == 64 || w == 128 || w == 256; }
 
 template <class H>
 int sip_dispatch_ragged(const H& h, const uint8_t* buf, const u64* off, const u32* lens, u64 n,
-                        u64* out, cudaStream_t st) {
+                        u64* out, cudaStream_t st, bool staged = false) {
+  if (staged) return launch_staged_any(h, buf, off, lens, 0, n, out, st);
   // The register-ring reader is the Sip ragged kernel at every length: its
   // alignment-branch-free word reads beat the prefetching direct reader even
   // on short keys (cfg3-shaped SipHash-2-4: 2.86 vs 3.91 ms).
@@ -1301,27 +1413,29 @@ int lh_siphash_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
   if (!key || c < 1 || d < 1 || (n && (!d_out || !d_offsets || !d_buf))) return LH_EINVAL;
   if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4)
     return LH_EALIGN;
-  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT && kernel != LH_KERNEL_RING)
+  if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT && kernel != LH_KERNEL_RING &&
+      kernel != LH_KERNEL_STAGED)
     return LH_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool staged = kernel == LH_KERNEL_STAGED;
   if (tree) {
     if (c == 2 && d == 4)
       return sip_dispatch_ragged(make_siptree<2, 4>(key, c, d), d_buf, d_offsets, d_lengths, n,
-                                 d_out, st);
+                                 d_out, st, staged);
     if (c == 1 && d == 3)
       return sip_dispatch_ragged(make_siptree<1, 3>(key, c, d), d_buf, d_offsets, d_lengths, n,
-                                 d_out, st);
+                                 d_out, st, staged);
     return sip_dispatch_ragged(make_siptree<0, 0>(key, c, d), d_buf, d_offsets, d_lengths, n,
-                               d_out, st);
+                               d_out, st, staged);
   }
   if (c == 2 && d == 4)
     return sip_dispatch_ragged(make_sip<2, 4>(key, c, d), d_buf, d_offsets, d_lengths, n, d_out,
-                               st);
+                               st, staged);
   if (c == 1 && d == 3)
     return sip_dispatch_ragged(make_sip<1, 3>(key, c, d), d_buf, d_offsets, d_lengths, n, d_out,
-                               st);
+                               st, staged);
   return sip_dispatch_ragged(make_sip<0, 0>(key, c, d), d_buf, d_offsets, d_lengths, n, d_out,
-                             st);
+                             st, staged);
 }
 
 int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,

@@ -47,6 +47,9 @@ HOST_CHUNK_BYTES = 128 << 20
 # this use the register-ring kernel (KERNEL_RING): several packets in flight
 # per thread; shorter ones the warp-staged short-key kernel.
 RING_MIN_MEAN_BYTES = 128
+# Sip-family ragged batches below this mean length use the warp-staged kernel
+# (cfg3-shaped SipHash-1-3 2.10 -> 1.70 ms); at a 128-B mean it loses to the ring.
+SIP_STAGED_MAX_MEAN_BYTES = 64
 
 
 # Per-call host work matters for small, launch-bound batches (cfg1: a 3.5 us
@@ -299,16 +302,18 @@ def _to_device(x, dtype, device):
 
 
 def _ragged_kernel(kind, kernel, span_bytes, n):
-    """Kernel for a ragged launch.  HighwayHash: KERNEL_DIRECT (register
-    ring) when the mean message length reaches RING_MIN_MEAN_BYTES, else the
-    warp-staged short-key kernel.  Sip: always the register ring."""
-    allowed = (KERNEL_DIRECT, KERNEL_RING, KERNEL_STAGED) if kind == "hh" else \
-        (KERNEL_DIRECT, KERNEL_RING)
+    """Kernel for a ragged launch.  HighwayHash: the register ring when the
+    mean message length reaches RING_MIN_MEAN_BYTES, else the warp-staged
+    short-key kernel.  Sip: warp-staged below SIP_STAGED_MAX_MEAN_BYTES,
+    else the register ring."""
+    allowed = (KERNEL_DIRECT, KERNEL_RING, KERNEL_STAGED)
     if kernel != KERNEL_AUTO:
         if kernel not in allowed:
             raise ValueError(f"ragged {kind} batches take KERNEL_AUTO or one of {allowed}")
         return kernel
-    if kind != "hh" or (n and span_bytes >= RING_MIN_MEAN_BYTES * n):
+    if kind != "hh":  # Sip: warp-staged keys below 64 B on average, else the ring
+        return KERNEL_STAGED if n and span_bytes < SIP_STAGED_MAX_MEAN_BYTES * n else KERNEL_RING
+    if n and span_bytes >= RING_MIN_MEAN_BYTES * n:
         return KERNEL_RING
     return KERNEL_STAGED
 

@@ -148,9 +148,10 @@ def main(mode: str) -> int:
                 lambda o: lib.lh_highway_ragged_kernel(p, d_off.data_ptr(), None, n, k4, 64, 4, o,
                                                        st, kern), n, 1, want)
         want = oracle.batch_ragged(oracle.ALG_SIPHASH, synth.key128(), buf, off, None, 1, 3)
-        run(f"ragged sip13 {name}",
-            lambda o: lib.lh_siphash_ragged(p, d_off.data_ptr(), None, n, k2, 1, 3, 0, o, st), n,
-            1, want)
+        for kern in (KERNEL_RING, KERNEL_STAGED):
+            run(f"ragged sip13 {name} k={kern}",
+                lambda o: lib.lh_siphash_ragged_kernel(p, d_off.data_ptr(), None, n, k2, 1, 3, 0, o,
+                                                       st, kern), n, 1, want)
     return 1 if bad else 0
 
 

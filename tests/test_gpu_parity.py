@@ -419,8 +419,8 @@ def test_ragged_ring_unaligned_device_buffer(oracle, shift):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("case", ["sweep", "long", "tiny"])
-@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT])
+@pytest.mark.parametrize("case", ["sweep", "long", "tiny", "scattered"])
+@pytest.mark.parametrize("kernel", [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING, KERNEL_STAGED])
 def test_ragged_kernels_sip(oracle, case, kernel):
     buf, off, lens = _ragged_layout(case)
     for alg, c, d, tree in ((oracle.ALG_SIPHASH, 2, 4, False), (oracle.ALG_SIPHASH, 1, 3, False),
@@ -435,7 +435,7 @@ def test_ragged_kernel_choice_rejects_unknown():
     with pytest.raises(ValueError):
         engine.highway_ragged(synth.key256(), buf, off, lens, kernel=KERNEL_TMA)
     with pytest.raises(ValueError):
-        engine.sip_ragged(synth.key128(), buf, off, lens, kernel=KERNEL_STAGED)
+        engine.sip_ragged(synth.key128(), buf, off, lens, kernel=KERNEL_SPLIT)
 
 
 @pytest.mark.parametrize("shift", [1, 3, 8, 13])
