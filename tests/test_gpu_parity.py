@@ -131,12 +131,13 @@ def test_fixed_rows_every_kernel(oracle, L):
         for kernel in kernels:
             got = to_u64(engine.highway_batch(key, d, width, rounds, kernel=kernel))
             assert np.array_equal(got, want), (L, kernel, width, rounds)
-    want = oracle.batch_fixed(oracle.ALG_SIPTREE, synth.key128(), msgs, 2, 4)
-    for kernel in (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING):
-        got = to_u64(engine.sip_batch(synth.key128(), d, 2, 4, True, kernel=kernel))
-        assert np.array_equal(got, want), (L, kernel)
+    for alg, tree in ((oracle.ALG_SIPTREE, True), (oracle.ALG_SIPHASH, False)):
+        want = oracle.batch_fixed(alg, synth.key128(), msgs, 2, 4)
+        for kernel in (KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING, KERNEL_STAGED):
+            got = to_u64(engine.sip_batch(synth.key128(), d, 2, 4, tree, kernel=kernel))
+            assert np.array_equal(got, want), (L, kernel, tree)
     with pytest.raises(ValueError):
-        engine.sip_batch(synth.key128(), d, 2, 4, kernel=KERNEL_STAGED)
+        engine.sip_batch(synth.key128(), d, 2, 4, kernel=KERNEL_SPLIT)
 
 
 @pytest.mark.parametrize("rounds", [0, 1, 2, 3, 5])

@@ -79,14 +79,12 @@ def test_random_fixed(oracle, seed):
         width = int(rng.choice([64, 128, 256]))
         rounds = int(rng.integers(0, 6))
         want = oracle.batch_fixed(oracle.ALG_HIGHWAY, key, m, width, rounds)
-        sip_kernels = [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING]
+        sip_kernels = [KERNEL_AUTO, KERNEL_DIRECT, KERNEL_RING, KERNEL_STAGED]
         if L >= 32 and L % 16 == 0:
             sip_kernels.append(KERNEL_TMA)
         kernels = list(sip_kernels)
         if L >= 128 and L % 128 == 0:
             kernels.append(KERNEL_SPLIT)
-        if L <= 64:
-            kernels.append(KERNEL_STAGED)
         for kernel in kernels:
             got = to_u64(engine.highway_batch(key, d, width, rounds, kernel=kernel))
             assert np.array_equal(got, want), (seed, kernel, n, L, width, rounds)
