@@ -1177,7 +1177,8 @@ int dispatch_untiled<Highway>(const Highway& proto, const uint8_t* msgs, u64 n, 
   return launch_direct(proto, msgs, nullptr, nullptr, len, n, out, st);
 }
 
-// SipHash (not SipTree) rows of 32..127 bytes: the register-ring
+// SipHash (not SipTree) rows of 64..127 bytes (shorter ones go to the
+// warp-staged kernel first, see SipFamily below): the register-ring
 // kernel beats the TMA ring by 8-25% (scripts/untiled_ab.py-style sweep,
 // SipHash-1-3 at 64 B 0.414 vs 0.522 ms per GiB); from 128 B,
 // and for SipTree at every length, the TMA kernel is faster.
