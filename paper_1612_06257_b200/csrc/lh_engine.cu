@@ -13,6 +13,8 @@
 //   k_ragged_short  short keys (ragged, or fixed rows <= 64 B): warp-staged
 //       byte spans, non-divergent Update slots; falls back to the direct
 //       reader.
+//   k_staged_any<H,WARPS,MPL>  the warp staging for the Sip family's short
+//       keys (ragged, or fixed rows of 12..63 B), 4 keys per lane.
 //   k_ragged_ring<H,D,16>  ragged batches of medium/long messages
 //       (HighwayHash), every ragged Sip batch and fixed rows TMA does not
 //       take: one thread per message, 16-byte word reads branch-free in the
