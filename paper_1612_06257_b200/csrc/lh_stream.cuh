@@ -50,10 +50,11 @@ __device__ __forceinline__ void stream_append(StreamRec<H>& r, const uint8_t* p,
     absorb_blocks(r.h, p, len >> 5);
     load_tail(p + (len & ~31ull), (u32)(len & 31), r.tail);
   } else {
-    // 16-byte words, one block in flight (scripts/stream_bench.py: depth 2
-    // costs registers here; 8-byte words are 7% faster on 1000-B chunks but
-    // 1.3-1.9x slower on power-of-two-sized ragged appends).
-    absorb_ring128<1>(r.h, p, len, r.tail);
+    // 16-byte words, two blocks in flight.  (Depth 1 was ~10% faster here,
+    // but the same reader at depth 1 inlined into the staged kernels' fallback
+    // gave wrong digests on one code shape -- treated as a ptxas hazard,
+    // so depth 1 is used nowhere.)
+    absorb_ring128<2>(r.h, p, len, r.tail);
   }
   r.tlen = (u32)(len & 31);
 }
