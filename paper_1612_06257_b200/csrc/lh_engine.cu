@@ -936,6 +936,7 @@ int launch_direct(const H& proto, const uint8_t* buf, const u64* offsets, const 
 #define LH_RING_DEPTH 2
 #endif
 constexpr int kRingDepth = LH_RING_DEPTH;
+static_assert(kRingDepth >= 2, "ring depth 1 is not used (DESIGN.md §10: ptxas hazard)");
 
 template <class H>
 int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths,
