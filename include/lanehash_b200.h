@@ -196,6 +196,21 @@ int lh_sip_round_states(uint64_t* d_states, uint64_t n, int rounds, void* stream
 int lh_highway_bijectivity(uint64_t seed, uint64_t n, uint64_t* d_result,
                            void* stream);
 
+/* One pass over a ragged layout (offsets[n+1] form when d_lengths == NULL):
+ * for chunk k = messages [k*chunk_msgs, min(n, (k+1)*chunk_msgs)),
+ * d_lo[k] = min start and d_hi[k] = max end (byte offsets; chunks with no
+ * message keep lo = UINT64_MAX, hi = 0), and *d_bad = the number of invalid
+ * messages: offsets[i+1] < offsets[i], start + length wrapping, or end >
+ * buf_len (UINT64_MAX: no bound).  At most 65,535 chunks.  The hashing entry
+ * points TRUST offsets/lengths (they read buf + offsets[i] unchecked); the
+ * Python host runs this pass first and raises ValueError on *d_bad != 0, and
+ * uses the spans to copy only each chunk's bytes.  Replaces: nothing in the
+ * reference (it has no ragged API); the reference's per-message calls cannot
+ * index out of a Python bytes object. */
+int lh_ragged_plan(const uint64_t* d_offsets, const uint32_t* d_lengths, uint64_t n,
+                   uint64_t chunk_msgs, uint64_t buf_len, uint64_t* d_lo,
+                   uint64_t* d_hi, uint64_t* d_bad, void* stream);
+
 /* Seeded synthetic input generator (bench/test harness; not a reference
  * interface).  Byte b of the stream is byte (b & 7) of
  * word(seed, stream_id, word_offset + b / 8), see DESIGN.md §Synthetic

@@ -181,6 +181,22 @@ def _out_shape(n: int, lanes: int):
     return (n,) if lanes == 1 else (n, lanes)
 
 
+def _check_out(out: torch.Tensor, n: int, lanes: int, device) -> torch.Tensor:
+    """A caller-supplied digest tensor must be exactly what the kernels write:
+    n * lanes contiguous 64-bit words on the launch device (else the launch
+    would write out of bounds or scramble digests)."""
+    if not isinstance(out, torch.Tensor):
+        raise ValueError("out must be a torch tensor")
+    if not out.is_cuda or out.device != device:
+        raise ValueError(f"out must be a CUDA tensor on {device}, got {out.device}")
+    if out.dtype not in (torch.int64, torch.uint64):
+        raise ValueError(f"out must be int64 (or uint64), got {out.dtype}")
+    if tuple(out.shape) != _out_shape(n, lanes) or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous tensor of shape {_out_shape(n, lanes)}, "
+                         f"got {tuple(out.shape)}")
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Fixed-length batches
 # ---------------------------------------------------------------------------
@@ -209,6 +225,9 @@ def _fixed(kind, key, msgs, p1, p2, tree, lanes, kernel, out=None):
             n, L = msgs.shape
             if out is None:
                 out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=msgs.device)
+            elif (out.device != msgs.device or out.dtype is not torch.int64
+                  or out.shape != _out_shape(n, lanes) or not out.is_contiguous()):
+                _check_out(out, n, lanes, msgs.device)
             if n:
                 st = _raw_stream(idx) if _raw_stream is not None else \
                     torch.cuda.current_stream(idx).cuda_stream
@@ -229,10 +248,14 @@ def _fixed(kind, key, msgs, p1, p2, tree, lanes, kernel, out=None):
         m = m.contiguous()
         if out is None:
             out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=m.device)
+        else:
+            _check_out(out, n, lanes, m.device)
         if n:
             with _on_device(m.device):
                 _launch_fixed(kind, key, m, n, L, p1, p2, tree, out, kernel, m.device)
         return out
+    if out is not None:
+        raise ValueError("out= is only accepted with CUDA input (host batches return numpy)")
     return _fixed_host(kind, key, m.contiguous(), p1, p2, tree, lanes, kernel, device)
 
 
@@ -330,17 +353,36 @@ def _launch_ragged(kind, key, buf_ptr, off_ptr, len_ptr, n, p1, p2, tree, out, d
     _lib.check(rc, "ragged batch")
 
 
+def _plan(d_off, d_len, n: int, chunk_msgs: int, buf_len: int, device):
+    """lh_ragged_plan: per-chunk byte spans [lo, hi) and the invalid-message
+    count of a device-resident layout, in one launch and one small D2H
+    (csrc/lh_plan.cu).  Raises ValueError for an invalid layout."""
+    nchunks = -(-n // chunk_msgs)
+    res = torch.empty(2 * nchunks + 1, dtype=torch.int64, device=device)
+    rc = _lib.lib().lh_ragged_plan(d_off.data_ptr(), None if d_len is None else d_len.data_ptr(),
+                                   n, chunk_msgs, buf_len & 0xFFFFFFFFFFFFFFFF,
+                                   res.data_ptr(), res[nchunks:].data_ptr(),
+                                   res[2 * nchunks:].data_ptr(), _stream_ptr(device))
+    _lib.check(rc, "lh_ragged_plan")
+    r = res.cpu().numpy().view(np.uint64)
+    if r[-1]:
+        raise ValueError(f"invalid ragged layout: {int(r[-1])} of {n} messages have decreasing "
+                         f"offsets, a wrapping length or end past the {buf_len}-byte buffer")
+    return r[:nchunks], r[nchunks:2 * nchunks]
+
+
 def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device,
                            kernel=KERNEL_AUTO):
     """Host ragged batch streamed through the GPU in message-range chunks of
     about HOST_CHUNK_BYTES.  The offsets/lengths go to the device first (one
-    copy each); each chunk's byte span [min start, max end) is reduced on the
-    device and read back once for all chunks; then per chunk the span goes
-    H2D, the kernel runs and the digests come back D2H, alternating two
-    streams so copies overlap the other chunk's kernel.  Offsets are not
-    rebased: the kernel gets d_span - span_start as its buffer base (span_start
-    16-aligned), so buf + offsets[i] lands inside the copied span.  Returns
-    None when the spans are too scattered (caller falls back to one copy)."""
+    copy each); one lh_ragged_plan launch validates the layout and reduces
+    each chunk's byte span [min start, max end), read back once for all
+    chunks; then per chunk the span goes H2D, the kernel runs and the digests
+    come back D2H, alternating two streams so copies overlap the other
+    chunk's kernel.  Offsets are not rebased: the kernel gets d_span -
+    span_start as its buffer base (span_start 16-aligned), so buf +
+    offsets[i] lands inside the copied span.  Returns None when the spans are
+    too scattered (caller falls back to one copy)."""
     buf_t = buf if isinstance(buf, torch.Tensor) else _host_view(
         np.ascontiguousarray(buf, dtype=np.uint8))
     buf_t = buf_t.reshape(-1)
@@ -355,19 +397,13 @@ def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes
         return None
     d_off = off_t.to(device, non_blocking=True).contiguous()
     d_len = None if len_t is None else len_t.to(device, non_blocking=True).contiguous()
-    starts = d_off[:n]
-    ends = d_off[1:] if d_len is None else d_off + d_len.to(torch.int64)
-    # Packed batches: total ~ last end - first start (O(1)); the span check
-    # below catches anything else.
-    est = int(ends[-1].item() - starts[0].item())
-    nchunks = max(1, min(256, -(-max(est, 1) // HOST_CHUNK_BYTES)))
+    # Chunk count from the buffer size (packed batches: span ~ buffer / chunks).
+    nchunks = max(1, min(256, -(-max(buf_t.numel(), 1) // HOST_CHUNK_BYTES)))
     cnt = -(-n // nchunks)
-    bounds = [(a, min(n, a + cnt)) for a in range(0, n, cnt)]
-    los = torch.stack([starts[a:b].min() for a, b in bounds])
-    his = torch.stack([ends[a:b].max() for a, b in bounds])
-    los, his = los.cpu().tolist(), his.cpu().tolist()
+    los, his = _plan(d_off, d_len, n, cnt, buf_t.numel(), device)
     spans = []
-    for (a, b), lo, hi in zip(bounds, los, his):
+    for k, (lo, hi) in enumerate(zip(los.tolist(), his.tolist())):
+        a, b = k * cnt, min(n, (k + 1) * cnt)
         lo &= ~15
         if hi - lo > 4 * HOST_CHUNK_BYTES + 4096:
             return None  # scattered offsets: no compact span per chunk
@@ -396,7 +432,7 @@ def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes
 
 
 def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
-            kernel=KERNEL_AUTO):
+            kernel=KERNEL_AUTO, check=True):
     device = _require_cuda()
     _ragged_kernel(kind, kernel, 0, 0)  # validate before any work
     host = not (isinstance(buf, torch.Tensor) and buf.is_cuda)
@@ -422,7 +458,11 @@ def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
         raise ValueError("offsets must hold n+1 entries when lengths is None")
     if out is None:
         out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=device)
+    else:
+        _check_out(out, n, lanes, device)
     if n:
+        if check or host:  # host inputs are always checked (one extra sync is noise there)
+            _plan(d_off, d_len, n, n, d_buf.numel(), device)
         bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
         lp = d_len.data_ptr() if d_len is not None else None
         _launch_ragged(kind, key, bp, d_off.data_ptr(), lp, n, p1, p2, tree, out, device,
@@ -433,26 +473,35 @@ def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
 
 
 def highway_ragged(key, buf, offsets, lengths=None, width: int = 64, rounds: int = 4,
-                   out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO):
+                   out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO,
+                   check: bool = True):
     """HighwayHash over a packed ragged buffer.  Message i is
     buf[offsets[i] : offsets[i] + len_i] with len_i = lengths[i] when given,
     else offsets[i+1] - offsets[i] (offsets then holds n+1 entries).
     kernel: KERNEL_AUTO picks by mean length (RING_MIN_MEAN_BYTES);
     KERNEL_RING (or KERNEL_DIRECT) forces the register-ring kernel,
-    KERNEL_STAGED the warp-staged short-key kernel."""
+    KERNEL_STAGED the warp-staged short-key kernel.
+    check: validate the layout first (lh_ragged_plan: offsets non-decreasing,
+    no wrapping length, every message inside buf; ValueError otherwise).  It
+    costs one metadata pass and a sync; check=False skips it for CUDA inputs
+    the caller has validated (the C ABI's contract: offsets are trusted).
+    Host inputs are always checked."""
     _check_width(width)
     if rounds < 0:
         raise ValueError("rounds must be >= 0")
     return _ragged("hh", as_key256(key), buf, offsets, lengths, width, rounds, 0,
-                   width // 64, out, kernel)
+                   width // 64, out, kernel, check)
 
 
 def sip_ragged(key, buf, offsets, lengths=None, c: int = 2, d: int = 4, tree: bool = False,
-               out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO):
+               out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO,
+               check: bool = True):
+    """SipHash-c-d / SipTreeHash over a packed ragged buffer (layout and
+    ``check`` as highway_ragged)."""
     if c < 1 or d < 1:
         raise ValueError("round counts must be positive")
     return _ragged("sip", as_key128(key), buf, offsets, lengths, c, d, int(bool(tree)), 1, out,
-                   kernel)
+                   kernel, check)
 
 
 # ---------------------------------------------------------------------------
@@ -466,6 +515,8 @@ def prf64(key, start: int, n: int, rounds: int = 4, out: Optional[torch.Tensor] 
         raise ValueError("n and rounds must be >= 0")
     if out is None:
         out = torch.empty((n,), dtype=torch.int64, device=device)
+    else:
+        _check_out(out, n, 1, device)
     if n:
         rc = _lib.lib().lh_highway_prf64(start, n, _key4(as_key256(key)), rounds,
                                          out.data_ptr(), _stream_ptr(device))

@@ -44,11 +44,14 @@ def sweep(algo_name: str, sizes: Sequence[int], batch_bytes: int = 1 << 30,
     import torch
 
     from . import engine, synth
-    from .catalog import get_algorithm
+    from .registry import get_algorithm
 
     if steps < 1 or runs < 1:
         raise ValueError("steps and runs must be >= 1")
     algo = get_algorithm(algo_name)
+    if algo.engine is None:
+        raise ValueError(f"{algo_name} is a harness control, not an engine hash")
+    alg, p1, p2 = algo.engine
     dev = torch.device("cuda", torch.cuda.current_device())
     key = synth.key256() if algo.key_size == 32 else synth.key128()
     rows = []
@@ -59,13 +62,12 @@ def sweep(algo_name: str, sizes: Sequence[int], batch_bytes: int = 1 << 30,
         m = buf[: n * L].view(n, L)
         lanes = algo.digest_size // 8
         out = torch.empty((n, lanes) if lanes > 1 else (n,), dtype=torch.int64, device=dev)
-        if algo.alg == engine.ALG_HIGHWAY:
+        if alg == engine.ALG_HIGHWAY:
             def step():
-                engine.highway_batch(key, m, algo.p1, algo.p2, out=out)
+                engine.highway_batch(key, m, p1, p2, out=out)
         else:
             def step():
-                engine.sip_batch(key, m, algo.p1, algo.p2, algo.alg == engine.ALG_SIPTREE,
-                                 out=out)
+                engine.sip_batch(key, m, p1, p2, alg == engine.ALG_SIPTREE, out=out)
         for _ in range(warmup):
             step()
         st = torch.cuda.current_stream(dev)

@@ -1,12 +1,17 @@
-"""Full-size parity on BASELINE.json's configs (GPU).
+"""Full-size parity on BASELINE.json's configs (GPU): EVERY digest.
 
-At these sizes the CPU oracle cannot recheck every digest inside a test
-budget, so each config is checked by (a) the reference-generated golden
-prefix, (b) a seeded random sample of messages rechecked by the oracle, and
-(c) size-independent properties over ALL digests: two independent GPU code
-paths (TMA-staged vs direct-load kernels) agree bit-exactly, and hashing
-any split of the batch equals hashing it whole.
+Each full-size config is hashed on the device and every one of its digests
+is rechecked by the CPU oracle (oracle/lh_oracle.c on all host threads) on
+the same bytes, copied back from HBM: cfg3 2^26 short keys, cfg4 16,384 x
+1 MiB (HighwayHash-256), cfg5 2^24 x 1 KiB under HighwayHash-64 and all four
+Sip variants, PRF 2^28 counters.  The reference-generated golden prefixes
+(tests/golden/) are checked too, and the GPU kernels are also compared with
+each other (TMA / direct / split) -- that agreement is extra, not the proof.
+Protocol: the reference compares every case (T/test_acceptance.py:75-98;
+S/highway.py:247-254, S/sip.py:89-128).  Each test prints its oracle time.
 """
+import time
+
 import numpy as np
 import pytest
 import torch
@@ -31,6 +36,21 @@ def _fill(nbytes, seed):
     return t
 
 
+def _host(t):
+    """Device tensor -> numpy (bytes as the kernels saw them)."""
+    return t.cpu().numpy()
+
+
+def _mismatches(got, want, what):
+    bad = np.flatnonzero(np.any((got != want).reshape(len(got), -1), axis=1))
+    assert bad.size == 0, f"{what}: {bad.size} of {len(got)} digests differ, first at {bad[:8]}"
+
+
+def _log(name, n, t0):
+    print(f"\n[fullsize] {name}: {n} digests checked against the oracle in "
+          f"{time.perf_counter() - t0:.1f} s, 0 mismatches")
+
+
 def test_cfg3_short_keys_2p26(oracle):
     n = 1 << 26
     lens = torch.empty(n, dtype=torch.int32, device=DEV)
@@ -44,17 +64,11 @@ def test_cfg3_short_keys_2p26(oracle):
     assert torch.equal(d, dd)
     h = to_u64(d)
     assert np.array_equal(h[:8192], golden_npy("cfg3_first8192.npy"))
-    # split invariance: second half hashed alone
-    half = n // 2
-    d2 = engine.highway_ragged(synth.key256(), buf, off[half:-1], lens[half:], 64)
-    assert torch.equal(d2, d[half:])
-    # oracle recheck of a random sample
-    idx = np.sort(np.random.default_rng(33).choice(n, 1 << 16, replace=False))
-    off_h = off.cpu().numpy().view(np.uint64)
-    lens_h = lens.cpu().numpy().view(np.uint32)
-    buf_h = buf.cpu().numpy()
-    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), buf_h, off_h[idx], lens_h[idx], 64, 4)
-    assert np.array_equal(h[idx], want)
+    t0 = time.perf_counter()
+    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), _host(buf),
+                               _host(off).view(np.uint64), None, 64, 4)
+    _mismatches(h, want, "cfg3 HighwayHash-64")
+    _log("cfg3 hh64 2^26 ragged", n, t0)
 
 
 def test_cfg4_long_messages_16GiB(oracle, golden):
@@ -62,42 +76,50 @@ def test_cfg4_long_messages_16GiB(oracle, golden):
     buf = _fill(n * L, 5)
     m = buf.view(n, L)
     a = engine.highway_batch(synth.key256(), m, 256)  # auto: split-state kernel
-    b = engine.highway_batch(synth.key256(), m, 256, kernel=KERNEL_DIRECT)
     c = engine.highway_batch(synth.key256(), m, 256, kernel=KERNEL_TMA)
-    s = engine.highway_batch(synth.key256(), m, 256, kernel=KERNEL_SPLIT)
-    assert torch.equal(a, b) and torch.equal(a, c) and torch.equal(a, s)
+    assert torch.equal(a, c)
     h = to_u64(a)
     assert [f"{int(x):016x}" for x in h[0]] == golden["cfg4_msg0_h256"]
-    for i in (1, 777, n - 1):
-        row = m[i].cpu().numpy().reshape(1, L)
-        assert np.array_equal(h[i], oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), row,
-                                                       256, 4)[0])
+    t0 = time.perf_counter()
+    want = oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), _host(m), 256, 4)
+    _mismatches(h, want, "cfg4 HighwayHash-256")
+    _log("cfg4 hh256 16384 x 1 MiB", n, t0)
 
 
 def test_cfg5_comparators_2p24(oracle):
     n, L = 1 << 24, 1024
     buf = _fill(n * L, 6)
     m = buf.view(n, L)
+    host = _host(m)
     ref = np.load(GOLDEN + "/cfg5_first256.npz")
-    idx = np.sort(np.random.default_rng(55).choice(n, 2048, replace=False))
-    rows = m[torch.from_numpy(idx).to(DEV)].cpu().numpy()
-    # HighwayHash-64
-    a = engine.highway_batch(synth.key256(), m, 64, kernel=KERNEL_TMA)
-    b = engine.highway_batch(synth.key256(), m, 64, kernel=KERNEL_DIRECT)
-    assert torch.equal(a, b)
+    a = engine.highway_batch(synth.key256(), m, 64)
     h = to_u64(a)
     assert np.array_equal(h[:256], ref["hh64"])
-    assert np.array_equal(h[idx], oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), rows, 64, 4))
+    t0 = time.perf_counter()
+    _mismatches(h, oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), host, 64, 4), "hh64")
+    _log("cfg5 hh64 2^24 x 1 KiB", n, t0)
     for name, alg, c, d, tree in (("sip24", oracle.ALG_SIPHASH, 2, 4, False),
                                   ("sip13", oracle.ALG_SIPHASH, 1, 3, False),
                                   ("tree24", oracle.ALG_SIPTREE, 2, 4, True),
                                   ("tree13", oracle.ALG_SIPTREE, 1, 3, True)):
-        a = engine.sip_batch(synth.key128(), m, c, d, tree, kernel=KERNEL_TMA)
-        b = engine.sip_batch(synth.key128(), m, c, d, tree, kernel=KERNEL_DIRECT)
-        assert torch.equal(a, b), name
-        h = to_u64(a)
+        h = to_u64(engine.sip_batch(synth.key128(), m, c, d, tree))
         assert np.array_equal(h[:256], ref[name]), name
-        assert np.array_equal(h[idx], oracle.batch_fixed(alg, synth.key128(), rows, c, d)), name
+        t0 = time.perf_counter()
+        _mismatches(h, oracle.batch_fixed(alg, synth.key128(), host, c, d), name)
+        _log(f"cfg5 {name} 2^24 x 1 KiB", n, t0)
+
+
+def test_cfg5_kernels_agree_2p24():
+    """Extra (not the proof): the TMA and direct-load kernels agree on every
+    digest of the 16 GiB batch, for HighwayHash-64 and SipTree-1-3."""
+    n, L = 1 << 24, 1024
+    m = _fill(n * L, 6).view(n, L)
+    a = engine.highway_batch(synth.key256(), m, 64, kernel=KERNEL_TMA)
+    b = engine.highway_batch(synth.key256(), m, 64, kernel=KERNEL_DIRECT)
+    assert torch.equal(a, b)
+    a = engine.sip_batch(synth.key128(), m, 1, 3, True, kernel=KERNEL_TMA)
+    b = engine.sip_batch(synth.key128(), m, 1, 3, True, kernel=KERNEL_DIRECT)
+    assert torch.equal(a, b)
 
 
 def test_tma_large_batch_128row_config(oracle):
@@ -117,12 +139,11 @@ def test_tma_large_batch_128row_config(oracle):
 def test_prf_2p28(oracle):
     n = 1 << 28
     d = engine.prf64(synth.key256(), 0, n)
-    h = to_u64(d[:4096])
-    assert np.array_equal(h, golden_npy("prf_0_4096.npy"))
-    idx = np.random.default_rng(77).choice(n, 4096, replace=False)
-    hd = to_u64(d[torch.from_numpy(idx).to(DEV)])
-    want = np.array([oracle.prf64(synth.key256(), int(i), 1)[0] for i in idx], np.uint64)
-    assert np.array_equal(hd, want)
+    h = to_u64(d)
+    assert np.array_equal(h[:4096], golden_npy("prf_0_4096.npy"))
+    t0 = time.perf_counter()
+    _mismatches(h, oracle.prf64(synth.key256(), 0, n), "PRF")
+    _log("PRF 2^28 counters", n, t0)
     # window invariance over the tail of the range
     t = engine.prf64(synth.key256(), n - 100000, 100000)
     assert torch.equal(t, d[n - 100000:])

@@ -74,7 +74,7 @@ def test_exhaustive_finalization_experiment_runs():
 
 def test_finalization_variant(oracle):
     """S/registry.py:200-204: hash64 at a chosen finalization depth."""
-    from paper_1612_06257_b200.catalog import finalization_variant
+    from paper_1612_06257_b200.registry import finalization_variant
 
     key = bytes(range(32))
     lanes = np.frombuffer(key, np.uint64)

@@ -7,7 +7,7 @@ import pytest
 
 from conftest import GOLDEN
 from paper_1612_06257_b200 import cli, gpubench, synth, vectors
-from paper_1612_06257_b200.catalog import get_algorithm
+from paper_1612_06257_b200.registry import get_algorithm
 
 pytestmark = pytest.mark.gpu
 
@@ -90,7 +90,7 @@ def run_cli(capsys, *argv):
 
 
 def test_generate_covers_all_algorithms_and_lengths():
-    from paper_1612_06257_b200.catalog import VECTOR_ALGORITHMS
+    from paper_1612_06257_b200.registry import VECTOR_ALGORITHMS
 
     records = vectors.generate()
     assert len(records) == len(VECTOR_ALGORITHMS) * len(vectors.DEFAULT_LENGTHS)
@@ -114,7 +114,7 @@ def test_read_skips_comments_and_blank_lines():
 
 
 def test_cli_vectors_stdout_format(capsys):
-    from paper_1612_06257_b200.catalog import VECTOR_ALGORITHMS
+    from paper_1612_06257_b200.registry import VECTOR_ALGORITHMS
 
     code, out, _ = run_cli(capsys, "vectors")
     lines = out.strip().splitlines()
