@@ -461,7 +461,9 @@ def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
     else:
         _check_out(out, n, lanes, device)
     if n:
-        if check or host:  # host inputs are always checked (one extra sync is noise there)
+        # Host inputs are always checked (one extra sync is noise there).  A
+        # layout being captured into a CUDA graph cannot be read back: trusted.
+        if (check or host) and not torch.cuda.is_current_stream_capturing():
             _plan(d_off, d_len, n, n, d_buf.numel(), device)
         bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
         lp = d_len.data_ptr() if d_len is not None else None
@@ -485,7 +487,8 @@ def highway_ragged(key, buf, offsets, lengths=None, width: int = 64, rounds: int
     no wrapping length, every message inside buf; ValueError otherwise).  It
     costs one metadata pass and a sync; check=False skips it for CUDA inputs
     the caller has validated (the C ABI's contract: offsets are trusted).
-    Host inputs are always checked."""
+    Host inputs are always checked; calls captured into a CUDA graph are not
+    (nothing can be read back during capture)."""
     _check_width(width)
     if rounds < 0:
         raise ValueError("rounds must be >= 0")

@@ -1,14 +1,31 @@
-// intpeak.cu — integer-pipe ceilings on this B200 (tuning/roofline tool).
+// intpeak.cu — per-class integer throughput on this B200 (roofline tool).
 //
-//  1. alu:   independent LOP3/IADD3 chains (ALU pipe)       -> warp-instr/s
-//  2. prmt:  independent PRMT chains (ALU pipe)              -> warp-instr/s
-//  3. imadx: IMAD with carry chains (FMA pipe)               -> warp-instr/s
-//  4. wide:  IMAD.WIDE.U32 chains (FMA-heavy)                -> warp-instr/s
-//  5. update: the engine's HighwayHash Update (lh_device.cuh) on registers
-//     only, 1 thread per message, no memory traffic         -> Updates/s
-// The last number is the INT roof of the hash path: a launch of U Updates
-// can not finish faster than U / (Updates/s).  Prints JSON.
-// Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/intpeak tools/intpeak.cu
+// SURVEY.md §8(d) defines the integer roof of each hash as its canonical
+// 32-bit op mix divided by the measured rates of the SASS classes that mix
+// uses.  This program measures those rates: one kernel per class, each
+// thread running 8 independent dependence chains of a single instruction
+// (so the pipe, not latency, is the limit), 64 warps per SM on every SM.
+//
+//   iadd3   IADD3 a = a + b + c                 (ALU pipe)
+//   lop3    LOP3  a = a ^ b ^ c                 (ALU)
+//   prmt    PRMT  byte permute                  (ALU)
+//   shf     SHF.L.W funnel rotate               (ALU)
+//   imad    IMAD  a = a * b + c  (32-bit)        (FMA)
+//   wide    IMAD.WIDE.U32 32x32->64             (FMA, 64-bit result)
+//   add64   IADD3 + IADD3.X  (64-bit add, both halves on ALU)
+//   add64m  IADD3 + IMAD.X   (64-bit add, high half on FMA: the engine's form)
+// and 1:1 interleaved pairs, which show which classes share a pipe and the
+// dual-issue (instructions per clock) ceiling:
+//   prmt+lop3, prmt+imad, lop3+wide, shf+imad, iadd3+imad
+// plus the engine's full HighwayHash Update and SipRound on registers (the
+// achievable rates of the real instruction mixes).
+//
+// Output: one JSON object (warp-instructions per second per class, at the
+// SM clock sampled during the run).  The SASS of each kernel's loop is
+// checked by tools/intpeak_sass.py (one instruction per op).  The roofs per
+// hash are computed from this table by paper_1612_06257_b200/introof.py.
+// Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
+//            -o tools/intpeak tools/intpeak.cu   (run via tools/intpeak.py)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -18,67 +35,101 @@
 
 using namespace lh;
 
-__global__ void k_alu(u32* out, u32 seed, int iters) {
-  u32 a[8];
+enum Op { IADD3, LOP3, PRMT, SHF, IMAD, WIDE, ADD64, ADD64M, NOPS };
+static const char* kOpName[NOPS] = {"iadd3", "lop3", "prmt", "shf", "imad", "wide", "add64",
+                                    "add64m"};
+// SASS instructions one op issues (add64 / add64m are pairs).
+static const int kOpInstr[NOPS] = {1, 1, 1, 1, 1, 1, 2, 2};
+
+template <int OP>
+__device__ __forceinline__ void op32(u32& a, u32 b, u32 c) {
+  if (OP == IADD3) asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %0, %0, %2;" : "+r"(a) : "r"(b), "r"(c));
+  if (OP == LOP3) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a) : "r"(b), "r"(c));
+  if (OP == PRMT) asm volatile("prmt.b32 %0, %0, %1, 0x5041;" : "+r"(a) : "r"(b));
+  if (OP == SHF) asm volatile("shf.l.wrap.b32 %0, %0, %1, 13;" : "+r"(a) : "r"(b));
+  if (OP == IMAD) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a) : "r"(b), "r"(c));
+}
+
+// Single class: 8 chains x UNROLL steps per loop trip.
+template <int OP>
+__global__ void __launch_bounds__(256) k_class(u32* out, u32 seed, u32 one, int iters) {
+  constexpr int UNROLL = 16;
+  if (OP == WIDE || OP == ADD64 || OP == ADD64M) {
+    u64 a[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = seed ^ (threadIdx.x * 8 + k);
+    for (int k = 0; k < 8; ++k) a[k] = (u64)seed * (threadIdx.x + 8 * k + 1) + blockIdx.x;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int j = 0; j < UNROLL; ++j)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const u64 b = a[(k + 1) & 7];
+          if (OP == WIDE) a[k] = mul_lo_hi(a[k], b);
+          if (OP == ADD64M) a[k] = add64_mixed(a[k], b, one);
+          if (OP == ADD64) {
+            u32 lo, hi;
+            asm volatile("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+                         : "=r"(lo), "=r"(hi)
+                         : "r"(lo32(a[k])), "r"(lo32(b)), "r"(hi32(a[k])), "r"(hi32(b)));
+            a[k] = pack(lo, hi);
+          }
+        }
+    }
+    u64 s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= a[k];
+    if (s == 0x1234567ull) out[0] = (u32)s;
+  } else {
+    u32 a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed * (threadIdx.x + 8 * k + 1) + blockIdx.x;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int j = 0; j < UNROLL; ++j)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) op32<OP>(a[k], a[(k + 1) & 7], a[(k + 3) & 7]);
+    }
+    u32 s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= a[k];
+    if (s == 0x1234567u) out[0] = s;
+  }
+}
+
+// 1:1 pairs: chains 0-3 run class A, chains 4-7 class B.
+template <int A, int B>
+__global__ void __launch_bounds__(256) k_pair(u32* out, u32 seed, u32 one, int iters) {
+  constexpr int UNROLL = 16;
+  u32 a[8];
+  u64 w[4];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = seed * (threadIdx.x + 8 * k + 1) + blockIdx.x;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) w[k] = (u64)a[k] * 0x9E3779B97F4A7C15ull;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      a[k] = (a[k] ^ (a[(k + 1) & 7] + 0x9E3779B9u)) + a[(k + 3) & 7];
+    for (int j = 0; j < UNROLL; ++j) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) op32<A>(a[k], a[(k + 1) & 3], a[(k + 2) & 3]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (B == WIDE)
+          w[k] = mul_lo_hi(w[k], w[(k + 1) & 3]);
+        else
+          op32<B>(a[4 + k], a[4 + ((k + 1) & 3)], a[4 + ((k + 2) & 3)]);
+      }
     }
   }
   u32 s = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) s ^= a[k];
-  if (s == 0x12345678u) out[0] = s;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s ^= lo32(w[k]) ^ hi32(w[k]);
+  if (s == 0x1234567u) out[0] = s;
 }
 
-__global__ void k_prmt(u32* out, u32 seed, int iters) {
-  u32 a[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = seed ^ (threadIdx.x * 8 + k);
-  for (int i = 0; i < iters; ++i) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = __byte_perm(a[k], a[(k + 1) & 7], 0x5041);
-  }
-  u32 s = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s ^= a[k];
-  if (s == 0x12345678u) out[0] = s;
-}
-
-__global__ void k_wide(u64* out, u32 seed, int iters) {
-  u64 a[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 8 + k;
-  for (int i = 0; i < iters; ++i) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = mul_lo_hi(a[k], a[(k + 5) & 7] | (1ull << 40));
-  }
-  u64 s = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s ^= a[k];
-  if (s == 0x12345678u) out[0] = s;
-}
-
-__global__ void k_imadx(u64* out, u32 seed, u32 one, int iters) {
-  u64 a[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 8 + k;
-  for (int i = 0; i < iters; ++i) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = add64_mixed(a[k], a[(k + 3) & 7], one);
-  }
-  u64 s = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s ^= a[k];
-  if (s == 0x12345678u) out[0] = s;
-}
-
-// Packets come from shared memory with the same LDS.128 pattern as the
-// TMA kernel (2 per Update), so the SASS mix matches the real hot loop
-// minus the HBM stream.
+// The engine's HighwayHash Update on registers: 8 packets per trip from
+// shared memory (2 LDS.128 each, as the TMA kernel reads them).
 __global__ void __launch_bounds__(256) k_update(const Highway proto, u64* out, int iters) {
   __shared__ uint4 pk[8][256];
   for (int j = 0; j < 8; ++j)
@@ -98,53 +149,96 @@ __global__ void __launch_bounds__(256) k_update(const Highway proto, u64* out, i
   if (s == 0x12345678ull) out[0] = s;
 }
 
+// The engine's SipRound on registers, 2 independent states per thread.
+__global__ void __launch_bounds__(256) k_sipround(const SipMul km, u64* out, int iters) {
+  u64 v[2][4];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[s][k] = (u64)(threadIdx.x + 1) * (k + 3 + s) + blockIdx.x;
+  for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) sip_round(v[s][0], v[s][1], v[s][2], v[s][3], km);
+  }
+  u64 x = 0;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) x ^= v[s][0] ^ v[s][1] ^ v[s][2] ^ v[s][3];
+  if (x == 0x12345678ull) out[0] = x;
+}
+
 template <class F>
 static float time_ms(F f) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  f();
+  f();  // warm-up
   cudaDeviceSynchronize();
-  cudaEventRecord(a);
-  f();
-  cudaEventRecord(b);
-  cudaEventSynchronize(b);
-  float ms;
-  cudaEventElapsedTime(&ms, a, b);
-  return ms;
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(a);
+    f();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    best = ms < best ? ms : best;
+  }
+  return best;
+}
+
+static unsigned sm_clock_mhz() {
+  int v = 0;
+  // cudaDevAttrClockRate is the max clock; the live one comes from NVML in
+  // the driver script (scripts/intpeak.sh) -- here report the attribute.
+  cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, 0);
+  return (unsigned)(v / 1000);
 }
 
 int main() {
-  int sms;
+  int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  int clk_khz;
-  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
-  u64* d;
+  u32* d = nullptr;
   cudaMalloc(&d, 64);
-  const int blocks = sms * 8, threads = 256, iters = 4096;
+  const int blocks = sms * 8, threads = 256;  // 64 warps per SM
   const double warps = (double)blocks * threads / 32;
-  const double alu_instr = warps * iters * 8 * 2;  // LOP3 + IADD3 per chain step
-  float ms = time_ms([&] { k_alu<<<blocks, threads>>>((u32*)d, 7, iters); });
-  const double alu = alu_instr / (ms * 1e-3);
-  ms = time_ms([&] { k_prmt<<<blocks, threads>>>((u32*)d, 7, iters); });
-  const double prmt = warps * iters * 8 / (ms * 1e-3);
-  ms = time_ms([&] { k_wide<<<blocks, threads>>>(d, 7, iters); });
-  const double wide = warps * iters * 8 / (ms * 1e-3);
-  ms = time_ms([&] { k_imadx<<<blocks, threads>>>(d, 7, 1, iters); });
-  const double addm = warps * iters * 8 / (ms * 1e-3);  // IADD3 + IMAD.X pairs
+  const int iters = 512;                        // x 16 x 8 ops per thread
+  const double ops_per_warp = (double)iters * 16 * 8;
+  printf("{\"sms\": %d, \"clock_attr_mhz\": %u, \"warps_per_sm\": %d,\n", sms, sm_clock_mhz(),
+         blocks * threads / 32 / sms);
+  printf(" \"classes\": {");
+#define RUN_CLASS(OPV)                                                                         \
+  {                                                                                            \
+    const float ms = time_ms([&] { k_class<OPV><<<blocks, threads>>>(d, 7, 1, iters); });       \
+    const double r = warps * ops_per_warp * kOpInstr[OPV] / (ms * 1e-3);                      \
+    printf("%s\"%s\": {\"warp_instr_per_s\": %.5e, \"sass_per_op\": %d, \"ms\": %.4f}",        \
+           OPV ? ", " : "", kOpName[OPV], r, kOpInstr[OPV], ms);                               \
+  }
+  RUN_CLASS(IADD3) RUN_CLASS(LOP3) RUN_CLASS(PRMT) RUN_CLASS(SHF) RUN_CLASS(IMAD)
+  RUN_CLASS(WIDE) RUN_CLASS(ADD64) RUN_CLASS(ADD64M)
+  printf("},\n \"pairs\": {");
+#define RUN_PAIR(A, B, NAME, FIRST)                                                            \
+  {                                                                                            \
+    const float ms = time_ms([&] { k_pair<A, B><<<blocks, threads>>>(d, 7, 1, iters); });      \
+    const double r = warps * ops_per_warp / (ms * 1e-3);                                      \
+    printf("%s\"%s\": {\"warp_instr_per_s\": %.5e, \"ms\": %.4f}", FIRST ? "" : ", ", NAME, r,  \
+           ms);                                                                                \
+  }
+  RUN_PAIR(PRMT, LOP3, "prmt+lop3", 1) RUN_PAIR(PRMT, IMAD, "prmt+imad", 0)
+  RUN_PAIR(LOP3, WIDE, "lop3+wide", 0) RUN_PAIR(SHF, IMAD, "shf+imad", 0)
+  RUN_PAIR(IADD3, IMAD, "iadd3+imad", 0) RUN_PAIR(SHF, LOP3, "shf+lop3", 0)
+  printf("},\n");
   const u64 key[4] = {1, 2, 3, 4};
   const Highway proto = make_highway(key, 64, 4);
-  int ublocks = sms * 2;  // 16 warps per SM, as the bench kernel
-  const int uiters = 8192;
-  ms = time_ms([&] { k_update<<<ublocks, 256>>>(proto, d, uiters); });
+  const int ublocks = sms * 2, uiters = 8192;  // 16 warps per SM, as the bench kernel
+  float ms = time_ms([&] { k_update<<<ublocks, 256>>>(proto, (u64*)d, uiters); });
   const double updates = (double)ublocks * 256 * uiters / (ms * 1e-3);
-  printf("{\"sms\": %d, \"clock_khz_attr\": %d,\n", sms, clk_khz);
-  printf(" \"alu_warp_instr_per_s\": %.4e, \"alu_lane_ops_per_s\": %.4e,\n", alu, alu * 32);
-  printf(" \"prmt_warp_instr_per_s\": %.4e,\n", prmt);
-  printf(" \"imad_wide_warp_instr_per_s\": %.4e,\n", wide);
-  printf(" \"add64_mixed_pairs_warp_per_s\": %.4e,\n", addm);
-  printf(" \"highway_updates_per_s\": %.4e,\n", updates);
-  printf(" \"canonical_ops_per_update\": 80, \"ops_per_s\": %.4e,\n", updates * 80);
+  const SipMul km{1u, 1u << 13, 1u << 17, 1u << 21};
+  const int sblocks = sms * 8, siters = 4096;
+  ms = time_ms([&] { k_sipround<<<sblocks, 256>>>(km, (u64*)d, siters); });
+  const double sips = (double)sblocks * 256 * siters * 2 / (ms * 1e-3);
+  printf(" \"highway_update_per_s\": %.5e, \"sipround_per_s\": %.5e,\n", updates, sips);
   printf(" \"status\": \"%s\"}\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
