@@ -1,26 +1,41 @@
 #!/usr/bin/env python
 """Benchmark of the B200 keyed-hash engine (one JSON line on rank 0).
 
-Workload (BASELINE.json metric "HighwayHash GB/s hashed (1 KiB msgs)"):
-HighwayHash-64 over 2^24 messages x 1,024 bytes (16 GiB) per GPU — the
-roofline batch of SURVEY.md §8d, cfg1's message shape scaled up.  Inputs are
-generated in HBM by the seeded counter generator (seed 1; rank r holds
-messages [r*2^24, (r+1)*2^24) of the global batch), so they are resident
-before timing and 130x larger than L2 (no flush needed).  One step = one
-pass of the hot path over the whole per-GPU batch (one kernel launch).
+Headline workload (BASELINE.json metric "HighwayHash GB/s hashed (1 KiB
+msgs)"): HighwayHash-64 over 2^24 messages x 1,024 bytes (16 GiB) per GPU --
+SURVEY.md §8d's roofline batch, cfg1's message shape scaled up.  Inputs are
+generated in HBM by the seeded counter generator (seed 1) before timing and
+are 130x the L2 size, so no flush is needed.  One step = one launch of the
+hot path over the whole per-GPU batch.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--scaling weak|strong] [--no-configs]
+
+--gpus N > 1 without torchrun spawns N ranks itself (one process per GPU,
+NCCL); under torchrun WORLD_SIZE must equal N.  --scaling weak (default):
+2^24 messages per GPU; strong: a fixed global 2^24 x 1 KiB batch (and cfg4's
+16,384 x 1 MiB) split by message index (shard.fixed_shard).
+
+The line carries: the headline value and roofline (HBM against
+MEASURED_PEAKS.json; the read ceiling measured in this run; the integer roof
+from profiles/int_peak.json), burst and sustained (power-capped) regimes,
+e2e through the public API from pinned host memory (aggregate over ranks),
+the kernels actually launched (torch.profiler/CUPTI), and at N=1 one entry
+per BASELINE.json config (cfg1-cfg5, PRF, cfg4's 1/2/4/8-GPU shards) with
+its own roofline and CPU baseline.
 
 --impl reference times the reference algorithm's CPU implementation on the
-host cores (the oracle port oracle/lh_oracle.c with every available
-thread; the reference package itself is Python/numba and does not travel to
-the GPU box) on a bounded sample of the same workload.
+host cores (the oracle port oracle/lh_oracle.c on every thread; the
+reference package is Python/numba and does not travel to the GPU box) on
+the SAME workload: the full 2^24 x 1 KiB batch per step, generated on the
+host by the oracle's twin of the counter generator.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import sys
 import threading
 import time
@@ -36,8 +51,11 @@ MSG_BYTES = 1024
 N_MSGS = 1 << 24
 DIGEST_BYTES = 8
 DATA_SEED = 1
-CPU_SAMPLE_MSGS = 1 << 18  # 256 MiB per CPU step (~70 ms on 16 host threads)
 
+
+# ---------------------------------------------------------------------------
+# Measurement helpers
+# ---------------------------------------------------------------------------
 
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -49,25 +67,14 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def _traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/ncu_summary.json), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def _ncu_summary():
+    """The committed ncu --set full summary of the headline kernel
+    (profiles/ncu_summary.json), or {}."""
     try:
-        with open(p) as f:
-            j = json.load(f)
-        return j.get("bench_kernel", {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
-
-
-def _int_peak():
-    p = os.path.join(ROOT, "profiles", "int_peak.json")
-    try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             return json.load(f)
     except Exception:
-        return None
+        return {}
 
 
 class ClockSampler:
@@ -169,53 +176,6 @@ class ClockSampler:
         return out
 
 
-def _dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
-def cpu_baseline(steps: int, warmup: int = 1, nthreads=None, min_seconds: float = 0.0):
-    """Time the oracle port (all host threads) on CPU_SAMPLE_MSGS x 1 KiB of
-    the same workload (the first messages of rank 0's shard)."""
-    from oracle import oracle as orc
-    from paper_1612_06257_b200 import synth
-
-    threads = len(os.sched_getaffinity(0)) if nthreads is None else nthreads
-    msgs = synth.counter_bytes(DATA_SEED, CPU_SAMPLE_MSGS * MSG_BYTES).reshape(CPU_SAMPLE_MSGS,
-                                                                               MSG_BYTES)
-    key = synth.key256()
-    for _ in range(max(warmup, 1)):  # untimed warm-up passes
-        orc.batch_fixed(orc.ALG_HIGHWAY, key, msgs, 64, 4, nthreads=threads)
-    times = []
-    t_start = time.perf_counter()
-    while len(times) < steps or time.perf_counter() - t_start < min_seconds:
-        t0 = time.perf_counter()
-        orc.batch_fixed(orc.ALG_HIGHWAY, key, msgs, 64, 4, nthreads=threads)
-        times.append(time.perf_counter() - t0)
-    total = sum(times)
-    gbs = len(times) * CPU_SAMPLE_MSGS * MSG_BYTES / total / 1e9
-    # One core on a smaller slice, for the per-core figure SURVEY.md §8d asks for.
-    one = msgs[:CPU_SAMPLE_MSGS // 8]
-    t1, n1 = 0.0, 0
-    while t1 < 1.0:
-        t0 = time.perf_counter()
-        orc.batch_fixed(orc.ALG_HIGHWAY, key, one, 64, 4, nthreads=1)
-        t1 += time.perf_counter() - t0
-        n1 += 1
-    return {
-        "value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
-        "sample": f"{len(times)} passes x {CPU_SAMPLE_MSGS} msgs x {MSG_BYTES} B "
-                  f"(first messages of the bench batch), oracle/lh_oracle.c, {threads} threads, "
-                  f"{total:.2f} s",
-        "seconds": total,
-        "single_core": {"value": round(n1 * one.nbytes / t1 / 1e9, 3), "unit": UNIT,
-                        "sample": f"{n1} passes x {len(one)} msgs, 1 thread, {t1:.2f} s"},
-        "host": _host_info(),
-    }
-
-
 def _host_info():
     model = ""
     try:
@@ -230,54 +190,233 @@ def _host_info():
             "affinity": len(os.sched_getaffinity(0))}
 
 
-def len_or(k):
-    return max(1, k)
+def _threads():
+    return len(os.sched_getaffinity(0))
+
+
+def config_dict(ws: int, scaling: str, per_gpu: int) -> dict:
+    """The workload description both arms print (same keys and values)."""
+    return {"workload": "hh64_2^24x1KiB (HighwayHash-64, 2^24 messages x 1,024 B per GPU, SURVEY "
+                        "§8d roofline batch)" if scaling == "weak" else
+                        "hh64_2^24x1KiB_strong (HighwayHash-64, one global batch of 2^24 messages "
+                        "x 1,024 B split by message index)",
+            "messages_per_gpu": per_gpu, "global_messages": per_gpu * ws if scaling == "weak"
+            else N_MSGS, "msg_bytes": MSG_BYTES, "digest_bits": 64, "rounds": 4,
+            "parallelism": f"dp{ws} (message-index shards, no collective)",
+            "l2": "inputs 16 GiB per GPU >> 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------------------
+# Distributed control plane (NCCL on GPUs; gloo for the CPU test)
+# ---------------------------------------------------------------------------
+
+class Plane:
+    """Rank bookkeeping, barriers and max/sum over ranks.  World size 1 is a
+    no-op plane."""
+
+    def __init__(self, backend: str, device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.ws = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", str(self.rank)))
+        self.dist = dist if self.ws > 1 else None
+        self.device = device
+        if self.dist and not dist.is_initialized():
+            kw = {"device_id": device} if backend == "nccl" else {}
+            dist.init_process_group(backend, **kw)
+        self._t = lambda v: torch.tensor([float(v)], dtype=torch.float64,
+                                         device=device if backend == "nccl" else "cpu")
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def _reduce(self, v, op):
+        if not self.dist:
+            return float(v)
+        t = self._t(v)
+        self.dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    def max(self, v):
+        return self._reduce(v, self.dist.ReduceOp.MAX if self.dist else None)
+
+    def sum(self, v):
+        return self._reduce(v, self.dist.ReduceOp.SUM if self.dist else None)
+
+    def gather_u64(self, v: int):
+        """[v of rank 0, v of rank 1, ...] (u64 values)."""
+        if not self.dist:
+            return [v]
+        import torch
+
+        dev = self.device if self.device is not None else "cpu"
+        t = torch.tensor([np.array([v], np.uint64).view(np.int64)[0]], dtype=torch.int64,
+                         device=dev)
+        parts = [torch.zeros_like(t) for _ in range(self.ws)]
+        self.dist.all_gather(parts, t)
+        return [int(p.item()) & ((1 << 64) - 1) for p in parts]
+
+    def close(self):
+        if self.dist and self.dist.is_initialized():
+            self.dist.destroy_process_group()
+
+
+def headline_shard(ws: int, rank: int, scaling: str, n_per_gpu: int):
+    """[start, stop) of this rank's messages of the global batch."""
+    from paper_1612_06257_b200 import shard
+
+    if scaling == "weak":
+        return rank * n_per_gpu, (rank + 1) * n_per_gpu
+    return shard.fixed_shard(n_per_gpu, ws, rank)
+
+
+def summarise(plane: Plane, step_ms, total_ms: float, payload_bytes: int, steps: int,
+              scaling: str, global_payload: int):
+    """Whole-job value: bytes all ranks hashed / max-over-ranks time."""
+    t_max = plane.max(total_ms)
+    total_bytes = plane.sum(payload_bytes) if scaling == "weak" else global_payload
+    return {"value": total_bytes * steps / (t_max / 1e3) / 1e9, "t_max_ms": t_max,
+            "bytes_per_step": total_bytes}
+
+
+# ---------------------------------------------------------------------------
+# Reference arm: the CPU implementation on the same workload
+# ---------------------------------------------------------------------------
+
+def cpu_rate(fn, nbytes: int, min_seconds: float, min_passes: int = 1):
+    """Run fn until both min_passes and min_seconds are reached; GB/s."""
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < min_passes or time.perf_counter() - t_start < min_seconds:
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    return len(times) * nbytes / sum(times) / 1e9, len(times), sum(times)
 
 
 def run_reference(args):
-    ws, rank, _ = _dist_env()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cb = cpu_baseline(args.steps, warmup=args.warmup)
-    secs = cb["seconds"]
+    from oracle import oracle as orc
+    from paper_1612_06257_b200 import synth
+
+    threads = _threads()
+    n, L = args.msgs, MSG_BYTES
+    msgs = orc.synth_fill(n * L, DATA_SEED, nthreads=threads).reshape(n, L)
+    key = synth.key256()
+    for _ in range(max(args.warmup, 1)):
+        orc.batch_fixed(orc.ALG_HIGHWAY, key, msgs, 64, 4, nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.batch_fixed(orc.ALG_HIGHWAY, key, msgs, 64, 4, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    secs = sum(times)
+    gbs = args.steps * n * L / secs / 1e9
+    sample = (f"{args.steps} passes x {n} msgs x {L} B (the whole per-GPU batch, seed 1), "
+              f"oracle/lh_oracle.c on {threads} threads, {secs:.2f} s")
     line = {
-        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(secs / len_or(args.steps) * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (counter generator seed 1)",
-        "config": {"workload": f"hh64 over {CPU_SAMPLE_MSGS} x 1 KiB per step (bounded sample of "
-                               f"the 2^24 x 1 KiB batch)", "messages_per_step": CPU_SAMPLE_MSGS,
-                   "msg_bytes": MSG_BYTES, "digest_bits": 64},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
-                                             "single_core", "host")},
-        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+        "ms_per_step": round(secs / max(1, args.steps) * 1e3, 3), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (counter generator seed 1, generated on the host)",
+        "config": config_dict(1, args.scaling, n),
+        "cpu_baseline": {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample, "host": _host_info()},
+        "e2e": {"value": round(gbs, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "msgs_per_s": round(args.steps * n / secs, 1),
+        "checksum": f"{int(np.bitwise_xor.reduce(orc.batch_fixed(orc.ALG_HIGHWAY, key, msgs, 64, 4, nthreads=threads))):016x}",
     }
+    if ws > 1:
+        line["note"] = ("rank 0 alone runs the CPU implementation on one rank's batch; GB/s is "
+                        "per host, the GPU arm's value is the whole job")
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+
+def _kernels_of(fn):
+    """Names and count of the GPU kernels one call of fn launches (CUPTI via
+    torch.profiler, outside any timed region), or (None, None)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    try:
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events()
+                 if getattr(e, "device_type", None) is not None and
+                 str(e.device_type).endswith("CUDA") and "Memcpy" not in e.name
+                 and "Memset" not in e.name]
+        return names, len(names)
+    except Exception as exc:  # CUPTI unavailable: say so, do not guess
+        return [f"unavailable: {type(exc).__name__}"], None
+
+
+def _event_ms(fn, steps, warmup, stream):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
+        fn()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    return [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+
+
+def read_probe_gbs(buf, stream):
+    """HBM read ceiling measured now, on this buffer: lh_read_probe (16-byte
+    streaming loads), best of 5 launches."""
+    import torch
+
+    from paper_1612_06257_b200 import _lib
+
+    sink = torch.zeros(64, dtype=torch.int64, device=buf.device)
+    nbytes = buf.numel() & ~15
+
+    def go():
+        _lib.check(_lib.lib().lh_read_probe(buf.data_ptr(), nbytes, sink.data_ptr(),
+                                            stream.cuda_stream), "lh_read_probe")
+
+    ms = _event_ms(go, 5, 2, stream)
+    return nbytes / (min(ms) / 1e3) / 1e9
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
-    from paper_1612_06257_b200 import _lib, engine, synth
+    from paper_1612_06257_b200 import engine, introof, synth
 
-    ws, rank, local = _dist_env()
-    distributed = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # launched by torchrun
-    if distributed:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    local = int(os.environ.get("LOCAL_RANK", os.environ.get("RANK", "0")))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    plane = Plane("nccl", dev)
+    ws, rank = plane.ws, plane.rank
     key = synth.key256()
-    n, L = args.msgs, MSG_BYTES
+    L = MSG_BYTES
+    start, stop = headline_shard(ws, rank, args.scaling, args.msgs)
+    n = stop - start
     buf = torch.empty(n * L, dtype=torch.uint8, device=dev)
-    synth.fill_device(buf, DATA_SEED, word_offset=rank * n * L // 8)
+    synth.fill_device(buf, DATA_SEED, word_offset=start * L // 8)
     msgs = buf.view(n, L)
     out = torch.empty(n, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize()
 
     def step():
@@ -286,144 +425,258 @@ def run_ours(args):
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
-    if distributed:
-        dist.barrier()
+    plane.barrier()
     torch.cuda.synchronize()
-    stream = torch.cuda.current_stream(dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(torch.cuda.current_device(), enabled=not args.no_clock_sampler) as clk:
+    with ClockSampler(local, enabled=not args.no_clock_sampler) as clk:
         ev[0].record(stream)
         for i in range(args.steps):
             step()
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
-    if distributed:
-        dist.barrier()
+    plane.barrier()
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms_max = float(t.item())
+    s = summarise(plane, step_ms, total_ms, n * L, args.steps, args.scaling, N_MSGS * L)
+    value, t_max = s["value"], s["t_max_ms"]
+    fold = int(np.bitwise_xor.reduce(engine.to_u64(out)))
+    folds = plane.gather_u64(fold)
 
-    # checksum of checksums (validation only, outside the timed region)
-    fold_u = np.bitwise_xor.reduce(engine.to_u64(out))
-    fold = torch.tensor([int(np.array([fold_u], np.uint64).view(np.int64)[0])],
-                        dtype=torch.int64, device=dev)
-    folds = [fold.clone() for _ in range(ws)]
-    if distributed:
-        dist.all_gather(folds, fold)
-
-    payload = n * L
-    value = ws * payload * args.steps / (total_ms_max / 1e3) / 1e9
+    # --- what ran, and the roofs (outside the timed region) ---
+    names, per_step = _kernels_of(step)
+    sustained = None
+    if not args.no_sustained:
+        sus = _event_ms(step, args.sustained_steps, 0, stream)
+        k = min(20, len(sus) // 2)
+        with ClockSampler(local, enabled=not args.no_clock_sampler) as sclk:
+            tail = _event_ms(step, k, 0, stream)  # clocks of the capped regime
+        sustained = {"steps": len(sus) + k,
+                     "first20_ms": round(float(np.mean(sus[:k])), 4),
+                     "last20_ms": round(float(np.mean(tail)), 4),
+                     "first20_GB_per_s": round(n * L / np.mean(sus[:k]) / 1e6, 1),
+                     "last20_GB_per_s": round(n * L / np.mean(tail) / 1e6, 1),
+                     "last20_clocks": sclk.summary()}
+    read_gbs = read_probe_gbs(buf, stream)
     per_launch_ms = float(np.mean(step_ms))
     peak, peak_src = _peaks()
-    alg_bytes = payload + n * DIGEST_BYTES
+    alg_bytes = n * L + n * DIGEST_BYTES
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    ncu = _ncu_summary().get("bench_kernel", {})
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": _traffic(),
+            "frac": round(achieved / peak, 4),
+            "traffic": ncu.get("dram_bytes_per_launch"),
+            "traffic_source": ncu.get("source"),
             "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
-            "kernel": "k_tma_fixed<Highway,512,3,1>",
-            # north_star's nominal 8.0 TB/s HBM figure, reported beside the measured peak
-            "frac_of_nominal_8000": round(achieved / 8000.0, 4)}
-    intp = _int_peak()
-    if intp and intp.get("ops_per_s"):
-        ops = (80 * (L // 32 + 4) + 4) * n
-        int_t = ops / intp["ops_per_s"]
-        roof["int_pipe"] = {"canonical_ops_per_launch": ops, "peak_ops_per_s": intp["ops_per_s"],
-                            "t_int_ms": round(int_t * 1e3, 3),
-                            "frac": round(int_t / (per_launch_ms / 1e3), 4),
-                            "peak_source": "measured (profiles/int_peak.json, tools/intpeak.cu)"}
-        read_ceiling = 7260.0  # GB/s, TMA ring with a null consumer (profiles/r1_membench.txt)
-        roof["t_roof_ms"] = round(max(int_t, alg_bytes / (read_ceiling * 1e9)) * 1e3, 3)
-        roof["frac_of_max_hbm_read_or_int"] = round(roof["t_roof_ms"] / per_launch_ms, 4)
+            "kernel": names[0] if names else None,
+            "kernels_per_step": per_step,
+            "frac_of_nominal_8000": round(achieved / 8000.0, 4),
+            "read_ceiling_measured_gbs": round(read_gbs, 1),
+            "frac_of_measured_read_ceiling": round(achieved / read_gbs, 4)}
+    ir = introof.launch_roof(introof.highway_mix(L, 64), n)
+    if ir:
+        ir["frac_canonical"] = round(ir["t_int_canonical_ms"] / per_launch_ms, 4)
+        ir["frac_balanced"] = round(ir["t_int_balanced_ms"] / per_launch_ms, 4)
+        roof["int_pipe"] = ir
+        t_hbm = alg_bytes / (read_gbs * 1e9) * 1e3
+        roof["t_roof_ms"] = round(max(t_hbm, ir["t_int_balanced_ms"]), 4)
+        roof["frac_of_max_read_ceiling_or_int"] = round(roof["t_roof_ms"] / per_launch_ms, 4)
 
+    e2e = run_e2e(args, plane, key, dev, start, n)
     result = None
     if rank == 0:
         result = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(total_ms_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (counter generator seed 1, generated in HBM; rank r holds "
-                    "messages [r*2^24,(r+1)*2^24) of one global batch)",
-            "config": {"workload": "hh64_2^24x1KiB (HighwayHash-64, 2^24 messages x 1,024 B "
-                                   "per GPU, SURVEY §8d roofline batch)",
-                       "messages_per_gpu": n, "msg_bytes": L, "digest_bits": 64, "rounds": 4,
-                       "parallelism": f"dp{ws} (message-index shards, no collective)",
-                       "l2": "inputs 16 GiB per GPU >> 126 MB L2; no flush needed"},
-            "msgs_per_s": round(ws * n * args.steps / (total_ms_max / 1e3), 1),
+                    "messages [start_r, stop_r) of one global batch)",
+            "config": config_dict(ws, args.scaling, n),
+            "msgs_per_s": round(s["bytes_per_step"] / L * args.steps / (t_max / 1e3), 1),
             **({"steps_ms": [round(x, 3) for x in step_ms]} if args.dump_steps else {}),
             "step_ms": {"min": round(float(np.min(step_ms)), 4),
                         "median": round(float(np.median(step_ms)), 4),
                         "max": round(float(np.max(step_ms)), 4)},
+            "regimes": {"burst": {"steps": args.steps, "ms": round(per_launch_ms, 4),
+                                  "GB_per_s": round(n * L / per_launch_ms / 1e6, 1)},
+                        "sustained": sustained},
             "roofline": roof,
-            "gpu_launches": args.steps,
+            "gpu_launches": (per_step or 1) * args.steps,
             "clocks": clk.summary(),
-            "checksum": [f"{int(x.item()) & ((1 << 64) - 1):016x}" for x in folds],
+            "checksum": [f"{x:016x}" for x in folds],
+            "e2e": e2e,
         }
-    # e2e through the public API with host buffers (pinned), rank-local
-    e2e = run_e2e(args, key, dev, rank)
-    if distributed:
-        dist.barrier()
+    del buf, msgs, out
+    torch.cuda.empty_cache()
+    if args.scaling == "strong":
+        strong = strong_cfg4(args, plane, key, dev)
+        if rank == 0:
+            result["strong_cfg4"] = strong
+    if rank == 0 and ws == 1:
+        if not args.no_configs:
+            from scripts import bench_configs
+
+            result["configs"] = bench_configs.run_all(dev, args.config_steps, 3,
+                                                      cpu_seconds=args.config_cpu_seconds)
+        if not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline_headline(args.cpu_seconds)
+    plane.barrier()
     if rank == 0:
-        result["e2e"] = e2e
-        if ws == 1 and not args.no_cpu_baseline:
-            result["cpu_baseline"] = {k: v for k, v in cpu_baseline(
-                1, warmup=1, min_seconds=args.cpu_seconds).items() if k != "seconds"}
         print(json.dumps(result), flush=True)
-    if distributed:
-        dist.destroy_process_group()
+    plane.close()
     return 0
 
 
-def run_e2e(args, key, dev, rank):
-    """Same metric through engine.highway_batch() on a host-pinned batch:
-    every step copies the step's inputs H2D and the digests D2H."""
+def cpu_baseline_headline(min_seconds: float):
+    """The oracle port on every host thread over the first 2^22 messages
+    (4 GiB) of the headline batch, repeated for >= min_seconds; plus one core."""
+    from oracle import oracle as orc
+    from paper_1612_06257_b200 import synth
+
+    threads = _threads()
+    n = 1 << 22
+    msgs = orc.synth_fill(n * MSG_BYTES, DATA_SEED, nthreads=threads).reshape(n, MSG_BYTES)
+    key = synth.key256()
+    orc.batch_fixed(orc.ALG_HIGHWAY, key, msgs[: n // 8], 64, 4, nthreads=threads)
+    gbs, passes, secs = cpu_rate(
+        lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, msgs, 64, 4, nthreads=threads),
+        msgs.nbytes, min_seconds)
+    one = msgs[: 1 << 15]
+    g1, p1, s1 = cpu_rate(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, one, 64, 4, nthreads=1),
+                          one.nbytes, 1.0)
+    return {"value": round(gbs, 3), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{passes} passes x {n} msgs x {MSG_BYTES} B (first messages of the bench "
+                      f"batch), oracle/lh_oracle.c, {threads} threads, {secs:.2f} s",
+            "single_core": {"value": round(g1, 3), "unit": UNIT,
+                            "sample": f"{p1} passes x {len(one)} msgs, 1 thread, {s1:.2f} s"},
+            "host": _host_info()}
+
+
+def run_e2e(args, plane: Plane, key, dev, start: int, n_rank: int):
+    """The metric through the public API (engine.highway_batch on a pinned
+    host batch): every step copies the inputs H2D and the digests D2H.  N=1:
+    the whole headline batch (same config as the kernel and reference arms);
+    N>1: --e2e-msgs-multi per rank (host RAM).  Aggregate over ranks: bytes
+    all ranks hashed / max-over-ranks wall time."""
     import torch
 
     from paper_1612_06257_b200 import engine, synth
 
-    n, L = args.e2e_msgs, MSG_BYTES
+    n = min(n_rank, args.e2e_msgs if plane.ws == 1 else args.e2e_msgs_multi)
+    L = MSG_BYTES
     host = torch.empty((n, L), dtype=torch.uint8, pin_memory=True)
     tmp = torch.empty(n * L, dtype=torch.uint8, device=dev)
-    synth.fill_device(tmp, DATA_SEED, word_offset=rank * N_MSGS * L // 8)
+    synth.fill_device(tmp, DATA_SEED, word_offset=start * L // 8)
     host.view(-1).copy_(tmp)
     del tmp
     torch.cuda.empty_cache()
     for _ in range(max(1, min(args.warmup, 2))):
         engine.highway_batch(key, host, 64)
     steps = max(1, min(args.steps, args.e2e_steps))
+    plane.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         d = engine.highway_batch(key, host, 64)
     dt = time.perf_counter() - t0
     assert d.shape == (n,)
-    return {"value": round(n * L * steps / dt / 1e9, 2), "unit": UNIT,
-            "h2d_bytes_per_step": n * L, "d2h_bytes_per_step": n * DIGEST_BYTES,
-            "steps": steps, "messages_per_step": n,
+    dt_max = plane.max(dt)
+    total = plane.sum(n * L)
+    del host
+    return {"value": round(total * steps / dt_max / 1e9, 2), "unit": UNIT,
+            "h2d_bytes_per_step": int(total), "d2h_bytes_per_step": int(total // L * DIGEST_BYTES),
+            "steps": steps, "messages_per_step": int(total // L), "ranks": plane.ws,
             "path": "paper_1612_06257_b200.engine.highway_batch(key, pinned host (n,1024) uint8)"}
 
 
-def main(argv=None):
+def strong_cfg4(args, plane: Plane, key, dev):
+    """cfg4 (16,384 x 1 MiB, HighwayHash-256) split by message index across
+    the ranks: value = 16 GiB per step / max-over-ranks time."""
+    import torch
+
+    from paper_1612_06257_b200 import engine, shard, synth
+
+    n_all, L = 16384, 1 << 20
+    a, b = shard.fixed_shard(n_all, plane.ws, plane.rank)
+    buf = torch.empty((b - a) * L, dtype=torch.uint8, device=dev)
+    synth.fill_device(buf, 5, word_offset=a * L // 8)
+    m = buf.view(b - a, L)
+    o = torch.empty((b - a, 4), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    steps = max(3, args.steps // 2)
+    plane.barrier()
+    ms = _event_ms(lambda: engine.highway_batch(key, m, 256, out=o), steps, 2, stream)
+    t = plane.max(sum(ms))
+    del buf, m, o
+    torch.cuda.empty_cache()
+    return {"workload": "cfg4 16384 x 1 MiB hh256, strong (fixed global batch)",
+            "messages_per_rank": b - a, "ms": round(t / steps, 4),
+            "GB_per_s": round(n_all * L * steps / (t / 1e3) / 1e9, 1)}
+
+
+# ---------------------------------------------------------------------------
+# Process launch
+# ---------------------------------------------------------------------------
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawned(rank, argv, world, port, entry):
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
+                       "RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world)})
+    sys.exit(entry(parse(argv)) or 0)
+
+
+def spawn(args, argv, entry=None):
+    """--gpus N > 1 without torchrun: one process per GPU, ranks 0..N-1."""
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_spawned, args=(argv, args.gpus, _free_port(), entry or run_ours),
+                       nprocs=args.gpus, start_method="spawn")
+    return 0
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--msgs", type=int, default=N_MSGS)
-    ap.add_argument("--e2e-msgs", type=int, default=1 << 21)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-msgs", type=int, default=N_MSGS)
+    ap.add_argument("--e2e-msgs-multi", type=int, default=1 << 22)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--sustained-steps", type=int, default=150)
+    ap.add_argument("--config-steps", type=int, default=20)
+    ap.add_argument("--config-cpu-seconds", type=float, default=1.0)
+    ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clock-sampler", action="store_true")
     ap.add_argument("--dump-steps", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    return args
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
+    if "RANK" in os.environ:
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        if ws != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch with "
+                             f"torchrun --nproc-per-node {args.gpus}, or without torchrun")
+    elif args.gpus > 1:
+        return spawn(args, argv)
     return run_ours(args)
 
 

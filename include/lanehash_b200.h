@@ -222,6 +222,11 @@ int lh_synth_fill(uint8_t* d_buf, uint64_t nbytes, uint64_t seed,
 int lh_synth_lengths(uint32_t* d_len, uint64_t n, uint64_t seed,
                      uint64_t first, uint32_t lo, uint32_t hi, void* stream);
 
+/* Harness: stream-read nbytes (16-byte aligned; the tail past the last
+ * 16-byte unit is ignored) and XOR-fold them into d_sink[0..63] (zero it
+ * first).  bench.py times it to measure the HBM read ceiling in-run. */
+int lh_read_probe(const uint8_t* d_buf, uint64_t nbytes, uint64_t* d_sink, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

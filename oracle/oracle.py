@@ -54,6 +54,7 @@ def lib():
         l.lh_ref_hh_init.argtypes = [vp, vp]
         l.lh_ref_hh_remainder_packet.argtypes = [vp, ctypes.c_uint, vp]
         l.lh_ref_avalanche_counts.argtypes = [i32, vp, vp, u64, ctypes.c_uint32, i32, i32, vp, i32]
+        l.lh_ref_synth_fill.argtypes = [vp, u64, u64, u64, u64, i32]
         _lib = l
     return _lib
 
@@ -157,3 +158,13 @@ def avalanche_counts(alg, key, msgs: np.ndarray, p1: int, p2: int, nthreads=None
     if rc:
         raise ValueError("size too large")
     return out
+
+
+def synth_fill(nbytes: int, seed: int, word_offset: int = 0, stream: int = 0,
+               nthreads=None, out: np.ndarray = None) -> np.ndarray:
+    """Host twin of the engine's counter generator (synth.counter_bytes), on
+    all host threads: the reference leg's input, no GPU involved."""
+    buf = np.empty(max(nbytes, 1), np.uint8) if out is None else out
+    if nbytes:
+        lib().lh_ref_synth_fill(_ptr(buf), nbytes, seed, stream, word_offset, _threads(nthreads))
+    return buf[:nbytes]

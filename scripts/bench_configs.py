@@ -1,12 +1,21 @@
 #!/usr/bin/env python
-"""Device-resident throughput of every BASELINE.json config (one GPU).
+"""Device-resident throughput of every BASELINE.json config (one GPU), each
+with its roofline and the CPU baseline of the same config.
 
-Prints one JSON object per workload (and writes them to --out): GB/s of
-payload hashed, messages/s, per-launch ms (CUDA events on the launching
-stream, median of --steps after --warmup), and the HBM roofline fraction
-against MEASURED_PEAKS.json.  Inputs are generated in HBM by the seeded
-counter generator (paper_1612_06257_b200/synth.py).  Not the driver's bench
-(bench.py is); this is the per-config table in profiles/.
+``run_all`` is called by bench.py at N=1 (the ``configs`` array of its JSON
+line); run directly it prints one JSON object per workload.  Per workload:
+per-launch ms (CUDA events on the launching stream, median of ``steps``
+after ``warmup``), GB/s of payload, messages/s, the roofline that bounds it
+(HBM: algorithmic bytes / launch time against MEASURED_PEAKS.json; INT: the
+canonical-op roof of paper_1612_06257_b200/introof.py, canonical and
+pipe-balanced), the kernels launched (torch.profiler), and ``cpu_baseline``:
+the oracle port (oracle/lh_oracle.c, every host thread) on a bounded sample
+of the same config's inputs, repeated for >= cpu_seconds.
+
+Inputs: the seeded counter generator in HBM (synth.py; its host twin
+oracle.synth_fill for the CPU samples), seeds per SURVEY §8d.  Ragged
+launches use check=False: the layouts are generated here, and the timed
+quantity is the hashing kernel (the C ABI's contract).
 """
 from __future__ import annotations
 
@@ -20,12 +29,10 @@ import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
 
-from bench import ClockSampler  # noqa: E402
-from paper_1612_06257_b200 import engine, synth  # noqa: E402
-
-LAST_CLOCKS = {}  # NVML SM clock / throttle reasons of the last timed region
+from paper_1612_06257_b200 import engine, introof, synth  # noqa: E402
 
 
 def peak_gbs():
@@ -35,115 +42,90 @@ def peak_gbs():
         return 6650.0
 
 
-SETTLE_S = 2.0  # idle before each workload so none inherits the previous one's power-cap state
-
-
-def time_launch(fn, steps, warmup):
+def _time(fn, steps, warmup):
     torch.cuda.synchronize()
-    time.sleep(SETTLE_S)
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-    with ClockSampler(torch.cuda.current_device(), period=0.01) as clk:
-        ev[0].record(st)
-        for i in range(steps):
-            fn()
-            ev[i + 1].record(st)
-        torch.cuda.synchronize()
-    LAST_CLOCKS.clear()
-    LAST_CLOCKS.update(clk.summary())
-    ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
-    return float(np.median(ms)), float(np.min(ms))
+    ev[0].record(st)
+    for i in range(steps):
+        fn()
+        ev[i + 1].record(st)
+    torch.cuda.synchronize()
+    return float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]))
 
 
-def row(name, ms, payload, nmsgs, alg_bytes, note, extra=None):
+def _kernels(fn):
+    from bench import _kernels_of
+
+    names, count = _kernels_of(fn)
+    return names, count
+
+
+def _cpu(fn, nbytes, nmsgs, sample, seconds):
+    from bench import _threads, cpu_rate
+
+    fn()  # warm
+    gbs, passes, secs = cpu_rate(fn, nbytes, seconds)
+    return {"value": round(gbs, 3), "unit": "GB/s", "msgs_per_s": round(passes * nmsgs / secs, 1),
+            "cores": _threads(), "kind": "port",
+            "sample": f"{sample}; {passes} passes, {secs:.2f} s, oracle/lh_oracle.c"}
+
+
+def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound):
+    ms = _time(fn, steps, warmup)
+    names, count = _kernels(fn)
     pk = peak_gbs()
-    r = {"workload": name, "ms_median": round(ms, 4),
-         "GB_per_s": round(payload / ms / 1e6, 1),
+    hbm = alg_bytes / ms / 1e6
+    r = {"workload": name, "ms": round(ms, 4),
+         "GB_per_s": round(payload / ms / 1e6, 1) if payload else None,
          "msgs_per_s": round(nmsgs / ms * 1e3, 1),
-         "hbm_alg_bytes": alg_bytes,
-         "hbm_frac_of_measured_copy": round(alg_bytes / ms / 1e6 / pk, 4),
-         "note": note, "clocks": dict(LAST_CLOCKS)}
-    if extra:
-        r.update(extra)
+         "kernels": names, "launches_per_call": count,
+         "roofline": {"bound": bound, "hbm_achieved_gbs": round(hbm, 1), "hbm_peak_gbs": pk,
+                      "hbm_frac": round(hbm / pk, 4), "alg_bytes": alg_bytes}}
+    if mix is not None:
+        ir = introof.launch_roof(mix, nmsgs)
+        if ir:
+            ir["frac_canonical"] = round(ir["t_int_canonical_ms"] / ms, 4)
+            ir["frac_balanced"] = round(ir["t_int_balanced_ms"] / ms, 4)
+            r["roofline"]["int_pipe"] = ir
+    r["roofline"]["frac"] = (r["roofline"]["hbm_frac"] if bound == "hbm" else
+                             r["roofline"].get("int_pipe", {}).get("frac_balanced"))
+    r["cpu_baseline"] = cpu
+    print(json.dumps(r), flush=True)
     return r
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--only", default="")
-    ap.add_argument("--out", default="")
-    ap.add_argument("--settle", type=float, default=SETTLE_S)
-    a = ap.parse_args()
-    globals()["SETTLE_S"] = a.settle
-    dev = torch.device("cuda", 0)
+def _mean_mix(fn_mix, lengths):
+    """Per-message mean of a length-dependent mix over a length histogram."""
+    vals, counts = np.unique(lengths, return_counts=True)
+    m = introof.Mix()
+    for v, c in zip(vals.tolist(), counts.tolist()):
+        m.add(fn_mix(int(v)), c / len(lengths))
+    return m
+
+
+def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
+    from oracle import oracle as orc
+
     key, k128 = synth.key256(), synth.key128()
-    out = []
-    want = set(a.only.split(",")) if a.only else None
+    T = len(os.sched_getaffinity(0))
+    rows = []
 
     def on(n):
-        return want is None or n in want
+        return only is None or n in only
 
-    def emit(r):
-        print(json.dumps(r), flush=True)
-        out.append(r)
-
-    # cfg5-shaped 2^24 x 1 KiB batch (seed 6): HH64 + the Sip comparators
-    if on("cfg5") or on("hh64"):
-        n, L = 1 << 24, 1024
-        buf = torch.empty(n * L, dtype=torch.uint8, device=dev)
-        synth.fill_device(buf, 6)
-        m = buf.view(n, L)
-        o = torch.empty(n, dtype=torch.int64, device=dev)
-        ms, _ = time_launch(lambda: engine.highway_batch(key, m, 64, out=o), a.steps, a.warmup)
-        emit(row("hh64 2^24x1KiB", ms, n * L, n, n * L + 8 * n, "HBM/ALU"))
-        for name, c, d, tree in (("siphash24", 2, 4, False), ("siphash13", 1, 3, False),
-                                 ("siptree24", 2, 4, True), ("siptree13", 1, 3, True)):
-            ms, _ = time_launch(lambda: engine.sip_batch(k128, m, c, d, tree, out=o), a.steps,
-                                a.warmup)
-            emit(row(f"{name} 2^24x1KiB (cfg5)", ms, n * L, n, n * L + 8 * n, "INT-bound"))
-        for w in (128, 256):
-            o2 = torch.empty((n, w // 64), dtype=torch.int64, device=dev)
-            ms, _ = time_launch(lambda: engine.highway_batch(key, m, w, out=o2), a.steps, a.warmup)
-            emit(row(f"hh{w} 2^24x1KiB", ms, n * L, n, n * L + w // 8 * n, "HBM/ALU"))
-            del o2
-        del buf, m, o
-        torch.cuda.empty_cache()
-
-    if on("prf"):
-        n = 1 << 28
-        o = torch.empty(n, dtype=torch.int64, device=dev)
-        ms, _ = time_launch(lambda: engine.prf64(key, 0, n, out=o), a.steps, a.warmup)
-        emit(row("prf64 2^28 counters (cfg5)", ms, 0, n, 8 * n, "INT-bound (5 Updates/counter)"))
-        del o
-        torch.cuda.empty_cache()
-
-    if on("cfg3"):
-        n = 1 << 26
-        lens = torch.empty(n, dtype=torch.int32, device=dev)
-        synth.lengths_device(lens, 3, 8, 64)
-        off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-        off[1:] = torch.cumsum(lens.to(torch.int64), 0)
-        total = int(off[-1])
-        buf = torch.empty(total, dtype=torch.uint8, device=dev)
-        synth.fill_device(buf, 4)
-        o = torch.empty(n, dtype=torch.int64, device=dev)
-        offs = off[:-1]
-        ms, _ = time_launch(lambda: engine.highway_ragged(key, buf, offs, lens, 64, out=o),
-                            a.steps, a.warmup)
-        emit(row("cfg3 short keys 2^26 x U[8,64] (offsets+lengths)", ms, total, n,
-                 total + 12 * n + 8 * n, "INT-bound (finalization)"))
-        for name, c, d, tree in (("siphash24", 2, 4, False), ("siphash13", 1, 3, False)):
-            ms, _ = time_launch(lambda: engine.sip_ragged(k128, buf, offs, lens, c, d, tree, out=o),
-                                a.steps, a.warmup)
-            emit(row(f"cfg3-shaped short keys, {name} (ragged)", ms, total, n,
-                     total + 12 * n + 8 * n, "INT-bound"))
-        del buf, lens, off, o
-        torch.cuda.empty_cache()
+    if on("cfg1"):
+        h = synth.numpy_bytes(1, (4096, 1024))
+        msgs = torch.from_numpy(h).to(dev)
+        o = torch.empty(4096, dtype=torch.int64, device=dev)
+        cpu = _cpu(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, h, 64, 4, nthreads=T),
+                   h.nbytes, 4096, "cfg1 whole (4096 x 1 KiB)", cpu_seconds)
+        rows.append(_row("cfg1 4096 x 1 KiB hh64", lambda: engine.highway_batch(key, msgs, 64, out=o),
+                         steps * 5, warmup, h.nbytes, 4096, h.nbytes + 8 * 4096,
+                         introof.highway_mix(1024), cpu, "latency"))
 
     if on("cfg2"):
         b, off, lens = synth.remainder_sweep_bytes(2, 1024, 64)
@@ -152,78 +134,124 @@ def main():
         n = len(lens)
         for w in (64, 128, 256):
             o = torch.empty((n, w // 64) if w > 64 else (n,), dtype=torch.int64, device=dev)
-            ms, _ = time_launch(lambda: engine.highway_ragged(key, d_b, d_off, None, w, out=o),
-                                a.steps, a.warmup)
-            emit(row(f"cfg2 remainder sweep L=0..1023 x64 hh{w}", ms, len(b), n,
-                     len(b) + 8 * n + w // 8 * n, "L2-resident, launch-bound"))
+            cpu = _cpu(lambda: orc.batch_ragged(orc.ALG_HIGHWAY, key, b, off, None, w, 4,
+                                                nthreads=T),
+                       len(b), n, "cfg2 whole (65,536 ragged msgs)", cpu_seconds)
+            rows.append(_row(f"cfg2 remainder sweep L=0..1023 x64 hh{w}",
+                             lambda: engine.highway_ragged(key, d_b, d_off, None, w, out=o,
+                                                           check=False),
+                             steps * 5, warmup, len(b), n, len(b) + 8 * n + w // 8 * n,
+                             _mean_mix(lambda L: introof.highway_mix(L, w), lens), cpu, "latency"))
+
+    if on("cfg3"):
+        n = 1 << 26
+        lens = torch.empty(n, dtype=torch.int32, device=dev)
+        synth.lengths_device(lens, 3, 8, 64)
+        off = torch.zeros(n, dtype=torch.int64, device=dev)
+        off[1:] = torch.cumsum(lens[:-1].to(torch.int64), 0)
+        total = int(off[-1]) + int(lens[-1])
+        buf = torch.empty(total, dtype=torch.uint8, device=dev)
+        synth.fill_device(buf, 4)
+        o = torch.empty(n, dtype=torch.int64, device=dev)
+        hl = lens[: 1 << 22].cpu().numpy().view(np.uint32)
+        ho = off[: 1 << 22].cpu().numpy().view(np.uint64)
+        hb = orc.synth_fill(int(ho[-1]) + int(hl[-1]), 4, nthreads=T)
+        mix = _mean_mix(lambda L: introof.highway_mix(L, 64), hl)
+        cpu = _cpu(lambda: orc.batch_ragged(orc.ALG_HIGHWAY, key, hb, ho, hl, 64, 4, nthreads=T),
+                   len(hb), len(hl), "first 2^22 cfg3 keys", cpu_seconds)
+        rows.append(_row("cfg3 short keys 2^26 x U[8,64] hh64 (offsets+lengths)",
+                         lambda: engine.highway_ragged(key, buf, off, lens, 64, out=o, check=False),
+                         steps, warmup, total, n, total + 12 * n + 8 * n, mix, cpu, "int"))
+        for name, alg, c, d in (("siphash24", orc.ALG_SIPHASH, 2, 4),
+                                ("siphash13", orc.ALG_SIPHASH, 1, 3)):
+            cpu = _cpu(lambda: orc.batch_ragged(alg, k128, hb, ho, hl, c, d, nthreads=T),
+                       len(hb), len(hl), "first 2^22 cfg3 keys", cpu_seconds)
+            rows.append(_row(f"cfg3-shaped 2^26 short keys {name}",
+                             lambda: engine.sip_ragged(k128, buf, off, lens, c, d, out=o,
+                                                       check=False),
+                             steps, warmup, total, n, total + 20 * n,
+                             _mean_mix(lambda L: introof.sip_mix(L, c, d), hl), cpu, "int"))
+        del buf, lens, off, o
+        torch.cuda.empty_cache()
 
     if on("cfg4"):
-        n, L = 16384, 1 << 20
-        buf = torch.empty(n * L, dtype=torch.uint8, device=dev)
+        L = 1 << 20
+        h = orc.synth_fill(256 * L, 5, nthreads=T).reshape(256, L)
+        cpu = _cpu(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, h, 256, 4, nthreads=T), h.nbytes,
+                   256, "first 256 cfg4 messages (256 MiB)", cpu_seconds)
+        buf = torch.empty(16384 * L, dtype=torch.uint8, device=dev)
         synth.fill_device(buf, 5)
+        # The whole batch, then the per-GPU shard of a 2/4/8-GPU strong split.
+        for n in (16384, 8192, 4096, 2048):
+            m = buf[: n * L].view(n, L)
+            o = torch.empty((n, 4), dtype=torch.int64, device=dev)
+            r = _row(f"cfg4 {n} x 1 MiB hh256" + ("" if n == 16384 else
+                                                   f" (1/{16384 // n} shard of cfg4)"),
+                     lambda: engine.highway_batch(key, m, 256, out=o), max(3, steps // 2), 1,
+                     n * L, n, n * L + 32 * n, introof.highway_mix(L, 256), cpu, "hbm")
+            if n < 16384:
+                g = 16384 // n
+                r["strong_scaling_projection"] = {
+                    "gpus": g, "aggregate_GB_per_s": round(16384 * L / r["ms"] / 1e6, 1),
+                    "note": f"each of {g} GPUs hashes {n} messages; aggregate = 16 GiB / "
+                            f"shard time (no collective in the loop)"}
+            rows.append(r)
+        del buf
+        torch.cuda.empty_cache()
+
+    if on("cfg5"):
+        n, L = 1 << 24, 1024
+        buf = torch.empty(n * L, dtype=torch.uint8, device=dev)
+        synth.fill_device(buf, 6)
         m = buf.view(n, L)
-        o = torch.empty((n, 4), dtype=torch.int64, device=dev)
-        ms, _ = time_launch(lambda: engine.highway_batch(key, m, 256, out=o), max(3, a.steps // 4),
-                            1)
-        emit(row("cfg4 16384 x 1 MiB hh256", ms, n * L, n, n * L + 32 * n,
-                 "parallelism-starved: 16384 sequential chains"))
+        o = torch.empty(n, dtype=torch.int64, device=dev)
+        hs = orc.synth_fill((1 << 18) * L, 6, nthreads=T).reshape(1 << 18, L)
+        cpu = _cpu(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, hs, 64, 4, nthreads=T), hs.nbytes,
+                   len(hs), "first 2^18 cfg5 messages", cpu_seconds)
+        rows.append(_row("cfg5 hh64 2^24 x 1 KiB", lambda: engine.highway_batch(key, m, 64, out=o),
+                         steps, warmup, n * L, n, n * L + 8 * n, introof.highway_mix(L), cpu,
+                         "hbm"))
+        for name, alg, c, d, tree in (("siphash24", orc.ALG_SIPHASH, 2, 4, False),
+                                      ("siphash13", orc.ALG_SIPHASH, 1, 3, False),
+                                      ("siptree24", orc.ALG_SIPTREE, 2, 4, True),
+                                      ("siptree13", orc.ALG_SIPTREE, 1, 3, True)):
+            cpu = _cpu(lambda: orc.batch_fixed(alg, k128, hs, c, d, nthreads=T), hs.nbytes, len(hs),
+                       "first 2^18 cfg5 messages", cpu_seconds)
+            mix = introof.siptree_mix(L, c, d) if tree else introof.sip_mix(L, c, d)
+            t_hbm = (n * L + 8 * n) / (peak_gbs() * 1e9) * 1e3
+            t_int = (introof.launch_roof(mix, n) or {}).get("t_int_balanced_ms", 0)
+            rows.append(_row(f"cfg5 {name} 2^24 x 1 KiB",
+                             lambda: engine.sip_batch(k128, m, c, d, tree, out=o), steps, warmup,
+                             n * L, n, n * L + 8 * n, mix, cpu,
+                             "hbm" if t_hbm >= t_int else "int"))
         del buf, m, o
         torch.cuda.empty_cache()
 
-    if on("cfg1"):
-        msgs = torch.from_numpy(synth.numpy_bytes(1, (4096, 1024))).to(dev)
-        o = torch.empty(4096, dtype=torch.int64, device=dev)
-        ms, _ = time_launch(lambda: engine.highway_batch(key, msgs, 64, out=o), a.steps, a.warmup)
-        emit(row("cfg1 4096 x 1 KiB hh64", ms, 4096 * 1024, 4096, 4096 * 1032,
-                 "L2-resident, launch-bound"))
-        # The same call captured 32 times in a CUDA graph: the host launch
-        # cost (~9 us per Python call) leaves; the kernel's own time remains.
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for _ in range(32):
-                engine.highway_batch(key, msgs, 64, out=o)
-        ms, _ = time_launch(g.replay, max(3, a.steps // 4), 2)
-        emit(row("cfg1 4096 x 1 KiB hh64, CUDA-graph replay (per call)", ms / 32, 4096 * 1024,
-                 4096, 4096 * 1032, "kernel-bound: 36-Update chain per thread pair"))
+    if on("prf"):
+        n = 1 << 28
+        o = torch.empty(n, dtype=torch.int64, device=dev)
+        cpu = _cpu(lambda: orc.prf64(key, 0, 1 << 24, nthreads=T), 0, 1 << 24,
+                   "counters 0..2^24-1", cpu_seconds)
+        rows.append(_row("prf64 2^28 counters (cfg5)", lambda: engine.prf64(key, 0, n, out=o),
+                         steps, warmup, 0, n, 8 * n, introof.prf_mix(), cpu, "int"))
+        del o
+        torch.cuda.empty_cache()
+    return rows
 
-    if on("e2e"):
-        # End to end from pinned host memory through the public API (H2D, kernel, D2H).
-        n, L = 1 << 21, 1024
-        host = torch.empty((n, L), dtype=torch.uint8, pin_memory=True)
-        tmp = torch.empty(n * L, dtype=torch.uint8, device=dev)
-        synth.fill_device(tmp, 1)
-        host.view(-1).copy_(tmp)
-        del tmp
-        engine.highway_batch(key, host, 64)
-        t0 = time.perf_counter()
-        for _ in range(3):
-            engine.highway_batch(key, host, 64)
-        dt = (time.perf_counter() - t0) / 3
-        emit({"workload": "e2e hh64 2^21 x 1 KiB from pinned host", "ms": round(dt * 1e3, 2),
-              "GB_per_s": round(n * L / dt / 1e9, 2)})
-        m = 1 << 24  # cfg3-shaped ragged, host-resident (pinned)
-        lens = torch.empty(m, dtype=torch.int32, device=dev)
-        synth.lengths_device(lens, 3, 8, 64)
-        off = torch.zeros(m, dtype=torch.int64, device=dev)
-        off[1:] = torch.cumsum(lens.to(torch.int64), 0)[:-1]
-        total = int(off[-1] + lens[-1])
-        b = torch.empty(total, dtype=torch.uint8, device=dev)
-        synth.fill_device(b, 4)
-        hb, ho, hl = (t.cpu().pin_memory() for t in (b, off, lens))
-        del b, off, lens
-        engine.highway_ragged(key, hb, ho, hl, 64)
-        t0 = time.perf_counter()
-        for _ in range(3):
-            engine.highway_ragged(key, hb, ho, hl, 64)
-        dt = (time.perf_counter() - t0) / 3
-        emit({"workload": "e2e cfg3-shaped ragged 2^24 keys from pinned host", "ms": round(dt * 1e3, 2),
-              "GB_per_s_payload": round(total / dt / 1e9, 2),
-              "GB_per_s_incl_metadata": round((total + 12 * m) / dt / 1e9, 2),
-              "msgs_per_s": round(m / dt, 1)})
 
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--only", default="")
+    ap.add_argument("--cpu-seconds", type=float, default=1.0)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    rows = run_all(torch.device("cuda", 0), a.steps, a.warmup, a.cpu_seconds,
+                   set(a.only.split(",")) if a.only else None)
     if a.out:
         with open(a.out, "w") as f:
-            json.dump(out, f, indent=1)
+            json.dump(rows, f, indent=1)
 
 
 if __name__ == "__main__":
