@@ -345,24 +345,38 @@ def run_reference(args):
 # Our arm
 # ---------------------------------------------------------------------------
 
-def _kernels_of(fn):
-    """Names and count of the GPU kernels one call of fn launches (CUPTI via
-    torch.profiler, outside any timed region), or (None, None)."""
+def kernels_of_many(calls):
+    """{name: [kernel names]} for each (name, fn) in calls: the GPU kernels
+    one call of fn launches, from ONE torch.profiler (CUPTI) session outside
+    any timed region (a second session in the same process records nothing).
+    Each call runs alone between device syncs inside its own record_function
+    range; kernels are assigned to the range they start in."""
     import torch
-    from torch.profiler import ProfilerActivity, profile
+    from torch.profiler import ProfilerActivity, profile, record_function
 
     try:
         torch.cuda.synchronize()
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            fn()
-            torch.cuda.synchronize()
-        names = [e.name for e in prof.events()
-                 if getattr(e, "device_type", None) is not None and
-                 str(e.device_type).endswith("CUDA") and "Memcpy" not in e.name
-                 and "Memset" not in e.name]
-        return names, len(names)
+        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+            for name, fn in calls:
+                with record_function("lhcall::" + name):
+                    fn()
+                    torch.cuda.synchronize()
+        evs = prof.events()
+        ranges = sorted((e.time_range.start, e.time_range.end, e.name[len("lhcall::"):])
+                        for e in evs if e.name.startswith("lhcall::"))
+        out = {name: [] for name, _ in calls}
+        for e in evs:
+            if not str(getattr(e, "device_type", "")).endswith("CUDA"):
+                continue
+            if "Memcpy" in e.name or "Memset" in e.name or e.name.startswith("lhcall::"):
+                continue
+            t = e.time_range.start
+            owner = [r for r in ranges if r[0] <= t]
+            if owner:
+                out[owner[-1][2]].append(e.name)
+        return out
     except Exception as exc:  # CUPTI unavailable: say so, do not guess
-        return [f"unavailable: {type(exc).__name__}"], None
+        return {name: [f"unavailable: {type(exc).__name__}: {exc}"] for name, _ in calls}
 
 
 def _event_ms(fn, steps, warmup, stream):
@@ -443,7 +457,6 @@ def run_ours(args):
     folds = plane.gather_u64(fold)
 
     # --- what ran, and the roofs (outside the timed region) ---
-    names, per_step = _kernels_of(step)
     sustained = None
     if not args.no_sustained:
         sus = _event_ms(step, args.sustained_steps, 0, stream)
@@ -468,8 +481,7 @@ def run_ours(args):
             "traffic_source": ncu.get("source"),
             "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
-            "kernel": names[0] if names else None,
-            "kernels_per_step": per_step,
+            "kernel": None, "kernels_per_step": None,
             "frac_of_nominal_8000": round(achieved / 8000.0, 4),
             "read_ceiling_measured_gbs": round(read_gbs, 1),
             "frac_of_measured_read_ceiling": round(achieved / read_gbs, 4)}
@@ -502,25 +514,37 @@ def run_ours(args):
                                   "GB_per_s": round(n * L / per_launch_ms / 1e6, 1)},
                         "sustained": sustained},
             "roofline": roof,
-            "gpu_launches": (per_step or 1) * args.steps,
+            "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "checksum": [f"{x:016x}" for x in folds],
             "e2e": e2e,
         }
-    del buf, msgs, out
-    torch.cuda.empty_cache()
     if args.scaling == "strong":
         strong = strong_cfg4(args, plane, key, dev)
         if rank == 0:
             result["strong_cfg4"] = strong
+    calls = [("headline", step)] if rank == 0 else []
     if rank == 0 and ws == 1:
         if not args.no_configs:
             from scripts import bench_configs
 
             result["configs"] = bench_configs.run_all(dev, args.config_steps, 3,
-                                                      cpu_seconds=args.config_cpu_seconds)
+                                                      cpu_seconds=args.config_cpu_seconds,
+                                                      calls=calls)
         if not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline_headline(args.cpu_seconds)
+    if rank == 0:
+        # The kernels each timed call launches (one CUPTI session, at the end).
+        kn = kernels_of_many(calls)
+        head = kn.get("headline", [])
+        roof["kernel"] = head[0] if head else None
+        roof["kernels_per_step"] = len(head)
+        result["gpu_launches"] = len(head) * args.steps
+        for row in result.get("configs", []):
+            row["kernels"] = kn.get(row["workload"], [])
+            row["launches_per_call"] = len(row["kernels"])
+    del buf, msgs, out
+    torch.cuda.empty_cache()
     plane.barrier()
     if rank == 0:
         print(json.dumps(result), flush=True)

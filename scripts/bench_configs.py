@@ -57,13 +57,6 @@ def _time(fn, steps, warmup):
     return float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]))
 
 
-def _kernels(fn):
-    from bench import _kernels_of
-
-    names, count = _kernels_of(fn)
-    return names, count
-
-
 def _cpu(fn, nbytes, nmsgs, sample, seconds):
     from bench import _threads, cpu_rate
 
@@ -74,15 +67,15 @@ def _cpu(fn, nbytes, nmsgs, sample, seconds):
             "sample": f"{sample}; {passes} passes, {secs:.2f} s, oracle/lh_oracle.c"}
 
 
-def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound):
+def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, calls, verbose):
     ms = _time(fn, steps, warmup)
-    names, count = _kernels(fn)
+    if calls is not None:  # kernel names: filled in after one profiler session (bench.py)
+        calls.append((name, fn))
     pk = peak_gbs()
     hbm = alg_bytes / ms / 1e6
     r = {"workload": name, "ms": round(ms, 4),
          "GB_per_s": round(payload / ms / 1e6, 1) if payload else None,
          "msgs_per_s": round(nmsgs / ms * 1e3, 1),
-         "kernels": names, "launches_per_call": count,
          "roofline": {"bound": bound, "hbm_achieved_gbs": round(hbm, 1), "hbm_peak_gbs": pk,
                       "hbm_frac": round(hbm / pk, 4), "alg_bytes": alg_bytes}}
     if mix is not None:
@@ -94,7 +87,8 @@ def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound):
     r["roofline"]["frac"] = (r["roofline"]["hbm_frac"] if bound == "hbm" else
                              r["roofline"].get("int_pipe", {}).get("frac_balanced"))
     r["cpu_baseline"] = cpu
-    print(json.dumps(r), flush=True)
+    if verbose:
+        print(json.dumps(r), flush=True)
     return r
 
 
@@ -107,8 +101,14 @@ def _mean_mix(fn_mix, lengths):
     return m
 
 
-def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
+def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, verbose=False):
+    """One row per config.  ``calls`` (a list) collects (workload, fn) so the
+    caller can profile every config's launches in one CUPTI session; inputs
+    stay alive through the closures until the caller drops the list."""
     from oracle import oracle as orc
+
+    def _row_(*a):
+        return _row(*a, calls, verbose)
 
     key, k128 = synth.key256(), synth.key128()
     T = len(os.sched_getaffinity(0))
@@ -123,7 +123,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
         o = torch.empty(4096, dtype=torch.int64, device=dev)
         cpu = _cpu(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, h, 64, 4, nthreads=T),
                    h.nbytes, 4096, "cfg1 whole (4096 x 1 KiB)", cpu_seconds)
-        rows.append(_row("cfg1 4096 x 1 KiB hh64", lambda: engine.highway_batch(key, msgs, 64, out=o),
+        rows.append(_row_("cfg1 4096 x 1 KiB hh64", lambda: engine.highway_batch(key, msgs, 64, out=o),
                          steps * 5, warmup, h.nbytes, 4096, h.nbytes + 8 * 4096,
                          introof.highway_mix(1024), cpu, "latency"))
 
@@ -137,7 +137,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
             cpu = _cpu(lambda: orc.batch_ragged(orc.ALG_HIGHWAY, key, b, off, None, w, 4,
                                                 nthreads=T),
                        len(b), n, "cfg2 whole (65,536 ragged msgs)", cpu_seconds)
-            rows.append(_row(f"cfg2 remainder sweep L=0..1023 x64 hh{w}",
+            rows.append(_row_(f"cfg2 remainder sweep L=0..1023 x64 hh{w}",
                              lambda: engine.highway_ragged(key, d_b, d_off, None, w, out=o,
                                                            check=False),
                              steps * 5, warmup, len(b), n, len(b) + 8 * n + w // 8 * n,
@@ -159,14 +159,14 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
         mix = _mean_mix(lambda L: introof.highway_mix(L, 64), hl)
         cpu = _cpu(lambda: orc.batch_ragged(orc.ALG_HIGHWAY, key, hb, ho, hl, 64, 4, nthreads=T),
                    len(hb), len(hl), "first 2^22 cfg3 keys", cpu_seconds)
-        rows.append(_row("cfg3 short keys 2^26 x U[8,64] hh64 (offsets+lengths)",
+        rows.append(_row_("cfg3 short keys 2^26 x U[8,64] hh64 (offsets+lengths)",
                          lambda: engine.highway_ragged(key, buf, off, lens, 64, out=o, check=False),
                          steps, warmup, total, n, total + 12 * n + 8 * n, mix, cpu, "int"))
         for name, alg, c, d in (("siphash24", orc.ALG_SIPHASH, 2, 4),
                                 ("siphash13", orc.ALG_SIPHASH, 1, 3)):
             cpu = _cpu(lambda: orc.batch_ragged(alg, k128, hb, ho, hl, c, d, nthreads=T),
                        len(hb), len(hl), "first 2^22 cfg3 keys", cpu_seconds)
-            rows.append(_row(f"cfg3-shaped 2^26 short keys {name}",
+            rows.append(_row_(f"cfg3-shaped 2^26 short keys {name}",
                              lambda: engine.sip_ragged(k128, buf, off, lens, c, d, out=o,
                                                        check=False),
                              steps, warmup, total, n, total + 20 * n,
@@ -185,7 +185,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
         for n in (16384, 8192, 4096, 2048):
             m = buf[: n * L].view(n, L)
             o = torch.empty((n, 4), dtype=torch.int64, device=dev)
-            r = _row(f"cfg4 {n} x 1 MiB hh256" + ("" if n == 16384 else
+            r = _row_(f"cfg4 {n} x 1 MiB hh256" + ("" if n == 16384 else
                                                    f" (1/{16384 // n} shard of cfg4)"),
                      lambda: engine.highway_batch(key, m, 256, out=o), max(3, steps // 2), 1,
                      n * L, n, n * L + 32 * n, introof.highway_mix(L, 256), cpu, "hbm")
@@ -208,7 +208,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
         hs = orc.synth_fill((1 << 18) * L, 6, nthreads=T).reshape(1 << 18, L)
         cpu = _cpu(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, hs, 64, 4, nthreads=T), hs.nbytes,
                    len(hs), "first 2^18 cfg5 messages", cpu_seconds)
-        rows.append(_row("cfg5 hh64 2^24 x 1 KiB", lambda: engine.highway_batch(key, m, 64, out=o),
+        rows.append(_row_("cfg5 hh64 2^24 x 1 KiB", lambda: engine.highway_batch(key, m, 64, out=o),
                          steps, warmup, n * L, n, n * L + 8 * n, introof.highway_mix(L), cpu,
                          "hbm"))
         for name, alg, c, d, tree in (("siphash24", orc.ALG_SIPHASH, 2, 4, False),
@@ -220,7 +220,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
             mix = introof.siptree_mix(L, c, d) if tree else introof.sip_mix(L, c, d)
             t_hbm = (n * L + 8 * n) / (peak_gbs() * 1e9) * 1e3
             t_int = (introof.launch_roof(mix, n) or {}).get("t_int_balanced_ms", 0)
-            rows.append(_row(f"cfg5 {name} 2^24 x 1 KiB",
+            rows.append(_row_(f"cfg5 {name} 2^24 x 1 KiB",
                              lambda: engine.sip_batch(k128, m, c, d, tree, out=o), steps, warmup,
                              n * L, n, n * L + 8 * n, mix, cpu,
                              "hbm" if t_hbm >= t_int else "int"))
@@ -232,7 +232,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None):
         o = torch.empty(n, dtype=torch.int64, device=dev)
         cpu = _cpu(lambda: orc.prf64(key, 0, 1 << 24, nthreads=T), 0, 1 << 24,
                    "counters 0..2^24-1", cpu_seconds)
-        rows.append(_row("prf64 2^28 counters (cfg5)", lambda: engine.prf64(key, 0, n, out=o),
+        rows.append(_row_("prf64 2^28 counters (cfg5)", lambda: engine.prf64(key, 0, n, out=o),
                          steps, warmup, 0, n, 8 * n, introof.prf_mix(), cpu, "int"))
         del o
         torch.cuda.empty_cache()
@@ -248,7 +248,7 @@ def main():
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     rows = run_all(torch.device("cuda", 0), a.steps, a.warmup, a.cpu_seconds,
-                   set(a.only.split(",")) if a.only else None)
+                   set(a.only.split(",")) if a.only else None, verbose=True)
     if a.out:
         with open(a.out, "w") as f:
             json.dump(rows, f, indent=1)

@@ -66,8 +66,9 @@ def main():
         v["per_sm_per_clk"] = round(per_clk(v["warp_instr_per_s"]), 3)
     # Cross-pipe pairs (ALU class + FMA class) bound how many instructions
     # issue per clock; the best of them is the issue ceiling.
-    cross = ("prmt+imad", "lop3+wide", "shf+imad", "iadd3+imad")
-    issue = max(res["pairs"][p]["warp_instr_per_s"] for p in cross)
+    cross = ("prmt+imad", "lop3+imad", "shf+imad", "iadd3+imad")
+    issue = max([res["pairs"][p]["warp_instr_per_s"] for p in cross] +
+                [res["classes"][c]["warp_instr_per_s"] for c in ("add64", "add64m")])
     res.update({
         "sm_mhz": mhz, "clocks": cs,
         "issue_warp_instr_per_s": issue,
