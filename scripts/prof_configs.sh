@@ -4,7 +4,7 @@
 TAG=${1:-r1}
 prof() {  # name kernel-regex skip bench_configs-args...
   local name=$1 re=$2 skip=$3; shift 3
-  local CMD="python scripts/bench_configs.py --steps 1 --warmup 0 --settle 0 $*"
+  local CMD="python scripts/bench_configs.py --steps 1 --warmup 0 --cpu-seconds 0 $*"
   $CMD > gpurun_out/plain_$name.log 2>&1 && \
   ncu --set full --clock-control none -f -k regex:$re -s $skip -c 1 -o /tmp/prof_$name $CMD \
       > gpurun_out/ncu_$name.log 2>&1
