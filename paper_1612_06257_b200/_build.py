@@ -59,10 +59,12 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, so: str = SO, obj: str = OBJ) -> str:
+    """Compile and link.  ``so``/``obj`` redirect an A/B variant build
+    (LH_NVCC_EXTRA=-D...) away from the in-tree library."""
+    if not force and so == SO and not stale():
         return SO
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(obj, exist_ok=True)
     extra = os.environ.get("LH_NVCC_EXTRA", "").split()
     if verbose:
         extra += ["-Xptxas", "-v"]
@@ -72,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *FLAGS, *extra, *defs, "-c", src, "-o", obj]
         return subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True), cmd
 
-    units = _units()
+    units = [(os.path.join(obj, os.path.basename(o)), src, defs) for o, src, defs in _units()]
     with ThreadPoolExecutor(max_workers=min(len(units), os.cpu_count() or 4)) as pool:
         results = list(pool.map(compile_one, units))
     for r, cmd in results:
@@ -81,12 +83,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if r.returncode:
             raise subprocess.CalledProcessError(r.returncode, cmd, r.stdout, r.stderr)
     link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
-            "-o", SO + ".tmp", *[u[0] for u in units]]
+            "-o", so + ".tmp", *[u[0] for u in units]]
     subprocess.run(link, check=True, cwd=CSRC)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(SO)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--so", default=SO)
+    ap.add_argument("--obj", default=OBJ)
+    a = ap.parse_args()
+    print(build(force=True, verbose=a.v, so=os.path.abspath(a.so), obj=os.path.abspath(a.obj)))

@@ -254,7 +254,10 @@ __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
 // direct reader on mixed short/medium keys.  Depth 1 here
 // produced wrong digests for scattered offsets (a ptxas hazard like the one
 // noted above; the parity tests caught it), so it is not used.
-#define LH_STAGED_FALLBACK(h, p, l, o) hash_ring_any<2, 16>(h, p, l, o)
+#ifndef LH_FALLBACK_DEPTH
+#define LH_FALLBACK_DEPTH 2
+#endif
+#define LH_STAGED_FALLBACK(h, p, l, o) hash_ring_any<LH_FALLBACK_DEPTH, 16>(h, p, l, o)
 
 #ifndef LH_SHORT_MPL
 #define LH_SHORT_MPL 4
@@ -904,7 +907,10 @@ int launch_direct(const H& proto, const uint8_t* buf, const u64* offsets, const 
 #define LH_RING_DEPTH 2
 #endif
 constexpr int kRingDepth = LH_RING_DEPTH;
-static_assert(kRingDepth >= 2, "ring depth 1 is not used (DESIGN.md §10: ptxas hazard)");
+#ifndef LH_ALLOW_DEPTH1  // A/B builds only (tools/ring_depth1.sh)
+static_assert(kRingDepth >= 2 && LH_FALLBACK_DEPTH >= 2,
+              "ring depth 1 is not used (DESIGN.md §10)");
+#endif
 
 template <class H>
 int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths,
