@@ -24,6 +24,7 @@ import json
 import os
 import sys
 import time
+from functools import partial
 
 import numpy as np
 import torch
@@ -123,7 +124,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
         o = torch.empty(4096, dtype=torch.int64, device=dev)
         cpu = _cpu(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, h, 64, 4, nthreads=T),
                    h.nbytes, 4096, "cfg1 whole (4096 x 1 KiB)", cpu_seconds)
-        rows.append(_row_("cfg1 4096 x 1 KiB hh64", lambda: engine.highway_batch(key, msgs, 64, out=o),
+        rows.append(_row_("cfg1 4096 x 1 KiB hh64", partial(engine.highway_batch, key, msgs, 64, out=o),
                          steps * 5, warmup, h.nbytes, 4096, h.nbytes + 8 * 4096,
                          introof.highway_mix(1024), cpu, "latency"))
 
@@ -138,8 +139,8 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
                                                 nthreads=T),
                        len(b), n, "cfg2 whole (65,536 ragged msgs)", cpu_seconds)
             rows.append(_row_(f"cfg2 remainder sweep L=0..1023 x64 hh{w}",
-                             lambda: engine.highway_ragged(key, d_b, d_off, None, w, out=o,
-                                                           check=False),
+                             partial(engine.highway_ragged, key, d_b, d_off, None, w, out=o,
+                                     check=False),
                              steps * 5, warmup, len(b), n, len(b) + 8 * n + w // 8 * n,
                              _mean_mix(lambda L: introof.highway_mix(L, w), lens), cpu, "latency"))
 
@@ -160,19 +161,20 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
         cpu = _cpu(lambda: orc.batch_ragged(orc.ALG_HIGHWAY, key, hb, ho, hl, 64, 4, nthreads=T),
                    len(hb), len(hl), "first 2^22 cfg3 keys", cpu_seconds)
         rows.append(_row_("cfg3 short keys 2^26 x U[8,64] hh64 (offsets+lengths)",
-                         lambda: engine.highway_ragged(key, buf, off, lens, 64, out=o, check=False),
+                         partial(engine.highway_ragged, key, buf, off, lens, 64, out=o, check=False),
                          steps, warmup, total, n, total + 12 * n + 8 * n, mix, cpu, "int"))
         for name, alg, c, d in (("siphash24", orc.ALG_SIPHASH, 2, 4),
                                 ("siphash13", orc.ALG_SIPHASH, 1, 3)):
             cpu = _cpu(lambda: orc.batch_ragged(alg, k128, hb, ho, hl, c, d, nthreads=T),
                        len(hb), len(hl), "first 2^22 cfg3 keys", cpu_seconds)
             rows.append(_row_(f"cfg3-shaped 2^26 short keys {name}",
-                             lambda: engine.sip_ragged(k128, buf, off, lens, c, d, out=o,
-                                                       check=False),
+                             partial(engine.sip_ragged, k128, buf, off, lens, c, d, out=o,
+                                     check=False),
                              steps, warmup, total, n, total + 20 * n,
                              _mean_mix(lambda L: introof.sip_mix(L, c, d), hl), cpu, "int"))
-        del buf, lens, off, o
-        torch.cuda.empty_cache()
+        if calls is None:  # else the closures keep the inputs for the profiler pass
+            del buf, lens, off, o
+            torch.cuda.empty_cache()
 
     if on("cfg4"):
         L = 1 << 20
@@ -187,7 +189,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
             o = torch.empty((n, 4), dtype=torch.int64, device=dev)
             r = _row_(f"cfg4 {n} x 1 MiB hh256" + ("" if n == 16384 else
                                                    f" (1/{16384 // n} shard of cfg4)"),
-                     lambda: engine.highway_batch(key, m, 256, out=o), max(3, steps // 2), 1,
+                     partial(engine.highway_batch, key, m, 256, out=o), max(3, steps // 2), 1,
                      n * L, n, n * L + 32 * n, introof.highway_mix(L, 256), cpu, "hbm")
             if n < 16384:
                 g = 16384 // n
@@ -196,8 +198,9 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
                     "note": f"each of {g} GPUs hashes {n} messages; aggregate = 16 GiB / "
                             f"shard time (no collective in the loop)"}
             rows.append(r)
-        del buf
-        torch.cuda.empty_cache()
+        if calls is None:
+            del buf, m, o
+            torch.cuda.empty_cache()
 
     if on("cfg5"):
         n, L = 1 << 24, 1024
@@ -208,7 +211,7 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
         hs = orc.synth_fill((1 << 18) * L, 6, nthreads=T).reshape(1 << 18, L)
         cpu = _cpu(lambda: orc.batch_fixed(orc.ALG_HIGHWAY, key, hs, 64, 4, nthreads=T), hs.nbytes,
                    len(hs), "first 2^18 cfg5 messages", cpu_seconds)
-        rows.append(_row_("cfg5 hh64 2^24 x 1 KiB", lambda: engine.highway_batch(key, m, 64, out=o),
+        rows.append(_row_("cfg5 hh64 2^24 x 1 KiB", partial(engine.highway_batch, key, m, 64, out=o),
                          steps, warmup, n * L, n, n * L + 8 * n, introof.highway_mix(L), cpu,
                          "hbm"))
         for name, alg, c, d, tree in (("siphash24", orc.ALG_SIPHASH, 2, 4, False),
@@ -221,21 +224,20 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
             t_hbm = (n * L + 8 * n) / (peak_gbs() * 1e9) * 1e3
             t_int = (introof.launch_roof(mix, n) or {}).get("t_int_balanced_ms", 0)
             rows.append(_row_(f"cfg5 {name} 2^24 x 1 KiB",
-                             lambda: engine.sip_batch(k128, m, c, d, tree, out=o), steps, warmup,
+                             partial(engine.sip_batch, k128, m, c, d, tree, out=o), steps, warmup,
                              n * L, n, n * L + 8 * n, mix, cpu,
                              "hbm" if t_hbm >= t_int else "int"))
-        del buf, m, o
-        torch.cuda.empty_cache()
+        if calls is None:
+            del buf, m, o
+            torch.cuda.empty_cache()
 
     if on("prf"):
         n = 1 << 28
         o = torch.empty(n, dtype=torch.int64, device=dev)
         cpu = _cpu(lambda: orc.prf64(key, 0, 1 << 24, nthreads=T), 0, 1 << 24,
                    "counters 0..2^24-1", cpu_seconds)
-        rows.append(_row_("prf64 2^28 counters (cfg5)", lambda: engine.prf64(key, 0, n, out=o),
+        rows.append(_row_("prf64 2^28 counters (cfg5)", partial(engine.prf64, key, 0, n, out=o),
                          steps, warmup, 0, n, 8 * n, introof.prf_mix(), cpu, "int"))
-        del o
-        torch.cuda.empty_cache()
     return rows
 
 
