@@ -92,9 +92,10 @@ def prf_mix() -> Mix:
 def load_peaks(path: str = INT_PEAK) -> Optional[dict]:
     try:
         with open(path) as f:
-            return json.load(f)
+            j = json.load(f)
     except (OSError, ValueError):
         return None
+    return j if "classes" in j and "issue_warp_instr_per_s" in j else None
 
 
 def _times(mix: Mix, peaks: dict, hi_on_alu: float):
