@@ -111,6 +111,30 @@ struct Highway {
     update(p[0], p[1], p[2], p[3]);
   }
 
+  // The 16 state words from a copy of the prototype in shared memory (at
+  // shared address `sa`, 16-byte aligned, v0 v1 m0 m1 order) with 8
+  // LDS.128; the scalars from `proto`.  Kernels that start a new message
+  // every few hundred instructions use it instead of `h = proto`, which
+  // ptxas lowers to 16 LDCU.64 + 32 IMAD.U32 moves per message (the
+  // parameter lives in the constant bank).  The loads are volatile so they
+  // are not hoisted into 32 live registers.
+  __device__ __forceinline__ void load_state(u32 sa, const Highway& proto) {
+    u64* w[16] = {&v0[0], &v0[1], &v0[2], &v0[3], &v1[0], &v1[1], &v1[2], &v1[3],
+                  &m0[0], &m0[1], &m0[2], &m0[3], &m1[0], &m1[1], &m1[2], &m1[3]};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      u32 a, b, c, d;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                   : "r"(sa + 16 * k));
+      *w[2 * k] = pack(a, b);
+      *w[2 * k + 1] = pack(c, d);
+    }
+    rounds = proto.rounds;
+    width = proto.width;
+    one = proto.one;
+  }
+
   // S/highway.py:153-173: the exact inverse of update for the same packet
   // (self-test only; never on a hashing path).
   __device__ __forceinline__ void update_inverse(const u64 (&p)[4]) {
@@ -244,6 +268,25 @@ struct HighwayHalf {
     half = h;
   }
 
+  // This half's lanes from the shared-memory prototype (Highway::load_state
+  // layout: v0[4] v1[4] m0[4] m1[4]), 4 volatile LDS.128.
+  __device__ __forceinline__ void load_state(u32 sa, const Highway& full, u32 h) {
+    u64* w[8] = {&v0[0], &v0[1], &v1[0], &v1[1], &m0[0], &m0[1], &m1[0], &m1[1]};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      u32 a, b, c, d;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                   : "r"(sa + 32 * k + 16 * h));
+      *w[2 * k] = pack(a, b);
+      *w[2 * k + 1] = pack(c, d);
+    }
+    rounds = full.rounds;
+    width = full.width;
+    one = full.one;
+    half = h;
+  }
+
   __device__ __forceinline__ void update(u64 pa, u64 pb) {
     const u64 p[2] = {pa, pb};
 #pragma unroll
@@ -337,16 +380,17 @@ __device__ __forceinline__ u64 mulwide(u32 a, u32 b) {
   return r;
 }
 
-// Runtime constants that keep half of SipRound on the FMA pipe: `one` for
-// add64_mixed, and 2^13 / 2^17 (2^21 unused) so two of the four rotates become
-// IMAD.WIDE.U32 products (x * 2^k = x << k in the low word, x >> (32-k) in
-// the high word) merged by a 3-input LOP3 with the following XOR.  Set by
-// the host; opaque to ptxas, which would otherwise strength-reduce them.
+// Runtime constants that move part of SipRound to the FMA pipe: `one` for
+// add64_mixed, and 2^13 / 2^17 / 2^16 so those rotates become IMAD.WIDE.U32
+// products (x * 2^k = x << k in the low word, x >> (32-k) in the high word)
+// merged by a 3-input LOP3 with the following XOR.  Set by the host; opaque
+// to ptxas, which would otherwise strength-reduce them.
 struct SipMul {
-  u32 one, m13, m17, m21;
+  u32 one, m13, m17, m16;
 };
 
-// rotl64(x, k) ^ v with the shifts done as two 32x32->64 multiplies by 2^k.
+// rotl64(x, k) ^ v with the shifts done as two 32x32->64 multiplies by 2^k:
+// 2 IMAD.WIDE (FMA pipe) + 2 LOP3.
 __device__ __forceinline__ u64 rotl_xor_wide(u64 x, u32 pow2k, u64 v) {
   const u64 a = mulwide(lo32(x), pow2k), b = mulwide(hi32(x), pow2k);
   const u32 lo = (lo32(a) | hi32(b)) ^ lo32(v);
@@ -354,20 +398,65 @@ __device__ __forceinline__ u64 rotl_xor_wide(u64 x, u32 pow2k, u64 v) {
   return pack(lo, hi);
 }
 
-// S/sip.py:73-86.  ALU pipe: 4 IADD3 + 2 PRMT (rotate 16) + ~3 SHF (rotate
-// 21) + 8 LOP3; FMA pipe: 4 IMAD.X + 4 IMAD.WIDE (rotates 13, 17).  Moving
-// the rotate by 21 to IMAD.WIDE too measured slower (profiles/README.md).
+// rotl64(x, k) ^ v for 0 < k < 32 as two funnel shifts: 2 SHF + 2 LOP3 (ALU).
+template <int K>
+__device__ __forceinline__ u64 rotl_xor_shf(u64 x, u64 v) {
+  const u32 hi = __funnelshift_l(lo32(x), hi32(x), K);
+  const u32 lo = __funnelshift_l(hi32(x), lo32(x), K);
+  return pack(lo ^ lo32(v), hi ^ hi32(v));
+}
+
+// rotl64(x, 16) ^ v as two byte permutes: 2 PRMT + 2 LOP3 (ALU).
+__device__ __forceinline__ u64 rotl16_xor_prmt(u64 x, u64 v) {
+  const u32 lo = __byte_perm(hi32(x), lo32(x), 0x5432);
+  const u32 hi = __byte_perm(hi32(x), lo32(x), 0x1076);
+  return pack(lo ^ lo32(v), hi ^ hi32(v));
+}
+
+// S/sip.py:73-86.  The four 64-bit adds are IADD3 (ALU) + IMAD.X (FMA);
+// the rotates by 13 and 17 are IMAD.WIDE pairs (FMA), by 21 two SHF (ALU),
+// and by 16 two PRMT (W16 = false) or an IMAD.WIDE pair (W16 = true).  Per
+// round, in ALU / FMA issue slots: W16 = false 16 / 12, true 14 / 16;
+// alternating the two (sip_rounds) balances the pipes at 15 / 14 -- SipHash
+// is ALU-bound, so fewer ALU slots is time.
+template <bool W16>
 __device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k) {
   v0 = add64_mixed(v0, v1, k.one);
   v1 = rotl_xor_wide(v1, k.m13, v0);
   v0 = rot32(v0);
   v2 = add64_mixed(v2, v3, k.one);
-  v3 = rotl64(v3, 16) ^ v2;
+  v3 = W16 ? rotl_xor_wide(v3, k.m16, v2) : rotl16_xor_prmt(v3, v2);
   v0 = add64_mixed(v0, v3, k.one);
-  v3 = rotl64(v3, 21) ^ v0;
+  v3 = rotl_xor_shf<21>(v3, v0);
   v2 = add64_mixed(v2, v1, k.one);
   v1 = rotl_xor_wide(v1, k.m17, v2);
   v2 = rot32(v2);
+}
+
+__device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k) {
+  sip_round<false>(v0, v1, v2, v3, k);
+}
+
+// n SipRounds alternating the two pipe mixes (n compile-time when N > 0).
+template <int N>
+__device__ __forceinline__ void sip_rounds(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k,
+                                           int n) {
+  if (N > 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (i & 1)
+        sip_round<true>(v0, v1, v2, v3, k);
+      else
+        sip_round<false>(v0, v1, v2, v3, k);
+    }
+  } else {
+    int i = 0;
+    for (; i + 1 < n; i += 2) {
+      sip_round<false>(v0, v1, v2, v3, k);
+      sip_round<true>(v0, v1, v2, v3, k);
+    }
+    if (i < n) sip_round<false>(v0, v1, v2, v3, k);
+  }
 }
 
 struct SipKey {
@@ -386,23 +475,13 @@ struct SipCore {
   }
   __device__ __forceinline__ void compress(u64 m, int c, const SipMul& k) {
     v3 ^= m;
-    if (C > 0) {
-#pragma unroll
-      for (int i = 0; i < C; ++i) sip_round(v0, v1, v2, v3, k);
-    } else {
-      for (int i = 0; i < c; ++i) sip_round(v0, v1, v2, v3, k);
-    }
+    sip_rounds<C>(v0, v1, v2, v3, k, c);
     v0 ^= m;
   }
   __device__ __forceinline__ u64 final(u64 m_last, int c, int d, const SipMul& k) {
     compress(m_last, c, k);
     v2 ^= 0xFF;
-    if (D > 0) {
-#pragma unroll
-      for (int i = 0; i < D; ++i) sip_round(v0, v1, v2, v3, k);
-    } else {
-      for (int i = 0; i < d; ++i) sip_round(v0, v1, v2, v3, k);
-    }
+    sip_rounds<D>(v0, v1, v2, v3, k, d);
     return v0 ^ v1 ^ v2 ^ v3;
   }
 };

@@ -28,9 +28,18 @@ struct PrfProto {
 
 __global__ void __launch_bounds__(256) k_prf(const PrfProto proto, u64 start, u64 n,
                                              u64* __restrict__ out) {
+  __shared__ __align__(16) u64 s_state[16];  // proto.h's state (see Highway::load_state)
+  if (threadIdx.x < 16) {
+    const u64* src = threadIdx.x < 4 ? proto.h.v0 : threadIdx.x < 8 ? proto.h.v1
+                     : threadIdx.x < 12 ? proto.h.m0 : proto.h.m1;
+    s_state[threadIdx.x] = src[threadIdx.x & 3];
+  }
+  __syncthreads();
+  const u32 s_state_a = smem_u32(s_state);
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (u64)gridDim.x * blockDim.x) {
-    Highway h = proto.h;
+    Highway h;
+    h.load_state(s_state_a, proto.h);
     const u64 v1_0 = proto.v1_0_base + (start + i);         // steps 1-2
     h.m0[0] ^= (u64)lo32(v1_0) * (u64)proto.v0_0_hi;        // step 3
     h.m1[0] ^= mul_lo_hi(h.v0[0], v1_0);                    // step 5 (v0 post step 4)

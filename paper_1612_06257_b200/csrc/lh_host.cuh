@@ -49,7 +49,7 @@ inline Sip<C, D> make_sip(const u64 key[2], int c, int d) {
   h_sip_init(h.s, SipKey{key[0], key[1]});
   h.c = c;
   h.d = d;
-  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 21};
+  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 16};
   return h;
 }
 
@@ -65,7 +65,7 @@ inline SipTree<C, D> make_siptree(const u64 key[2], int c, int d) {
   h_sip_init(h.l3, k);
   h.c = c;
   h.d = d;
-  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 21};
+  h.k = SipMul{1u, 1u << 13, 1u << 17, 1u << 16};
   return h;
 }
 

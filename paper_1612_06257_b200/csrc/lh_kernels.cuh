@@ -67,6 +67,40 @@ __host__ __device__ inline int nout<Highway>(const Highway& h) {
   return h.width / 64;
 }
 
+// Prototype staging.  Every HighwayHash kernel starts each message from a
+// copy of the shared-memory prototype (Highway::load_state: 8 volatile
+// LDS.128) instead of `h = proto`.  Two reasons: `h = proto` costs 16
+// LDCU.64 + 32 IMAD.U32 per message (the parameter lives in the constant
+// bank), and ptxas (CUDA 12.9, sm_100a) has miscompiled finalization loops
+// that start from a parameter copy: it replaced the loop-carried v0[0] with
+// the parameter's c[0x0][0x380] (profiles/r2_depth1/).  A
+// value loaded by volatile LDS cannot be rematerialised from the constant
+// bank.  Other hashers copy the parameter as before.
+struct ProtoSmem {
+  u64 w[16];
+};
+
+__device__ __forceinline__ u32 stage_proto(const Highway& p, ProtoSmem& s) {
+  if (threadIdx.x < 16) {
+    const u32 t = threadIdx.x;
+    const u64* src = t < 4 ? p.v0 : t < 8 ? p.v1 : t < 12 ? p.m0 : p.m1;
+    s.w[t] = src[t & 3];
+  }
+  return smem_u32(&s);
+}
+template <class H>
+__device__ __forceinline__ u32 stage_proto(const H&, ProtoSmem& s) {
+  return smem_u32(&s);
+}
+
+__device__ __forceinline__ void init_state(Highway& h, const Highway& p, u32 sa) {
+  h.load_state(sa, p);
+}
+template <class H>
+__device__ __forceinline__ void init_state(H& h, const H& p, u32) {
+  h = p;
+}
+
 // PF: prefetch the next packet while hashing the current one (worth it for
 // messages of several packets; costs registers, so fixed batches of short
 // messages use PF = false).
@@ -174,6 +208,9 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
                                                 const u32* __restrict__ lengths, u64 fixed_len,
                                                 u64 n, u64* __restrict__ out) {
   const int W = nout(proto);
+  __shared__ __align__(16) ProtoSmem sp;
+  const u32 sa = stage_proto(proto, sp);
+  __syncthreads();
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (u64)gridDim.x * blockDim.x) {
     const uint8_t* msg;
@@ -186,7 +223,8 @@ __global__ void __launch_bounds__(256) k_direct(const H proto, const uint8_t* __
       msg = buf + i * fixed_len;
       len = fixed_len;
     }
-    H h = proto;
+    H h;
+    init_state(h, proto, sa);
     hash_direct<PF>(h, msg, len, out + i * W);
   }
 }
@@ -207,6 +245,9 @@ __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_
                                                      u64 fixed_len, u64 n,
                                                      u64* __restrict__ out) {
   const int W = nout(proto);
+  __shared__ __align__(16) ProtoSmem sp;
+  const u32 sa = stage_proto(proto, sp);
+  __syncthreads();
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (u64)gridDim.x * blockDim.x) {
     u64 off, len;
@@ -217,7 +258,8 @@ __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_
       off = i * fixed_len;
       len = fixed_len;
     }
-    H h = proto;
+    H h;
+    init_state(h, proto, sa);
     hash_ring_any<D, WORD>(h, buf + off, len, out + i * W);
   }
 }
@@ -273,9 +315,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
                                                              u64* __restrict__ out) {
   constexpr u32 kSpan = kSpanCap * MPL;
   __shared__ __align__(16) uint4 stage[WARPS][kSpan / 16 + 8];
+  __shared__ __align__(16) ProtoSmem sp;
   const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = proto.width / 64;
   const u32* S = reinterpret_cast<const u32*>(&stage[warp][0]);
+  const u32 s_state_a = stage_proto(proto, sp);
+  __syncthreads();
   for (u64 base = ((u64)blockIdx.x * WARPS + warp) * 32 * MPL; base < n;
        base += (u64)gridDim.x * WARPS * 32 * MPL) {
     u64 start[MPL], len[MPL];
@@ -325,7 +370,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
         const u32 nfull = L >> 5, r = L & 31;
         // Word k of the message (LE; bytes past L belong to other messages).
         auto word = [&](u32 k) { return __funnelshift_r(S[a + k], S[a + k + 1], sh); };
-        Highway h = proto;
+        Highway h;
+        h.load_state(s_state_a, proto);
         // Slot 0: block 0 if the message has one (32..64 bytes); no tweak.
         if (nfull) {
           u32 P[8];
@@ -358,7 +404,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       for (int m = 0; m < MPL; ++m) {
         const u64 i = base + 32 * m + lane;
         if (i < n) {
-          Highway h = proto;
+          Highway h;
+          h.load_state(s_state_a, proto);
           LH_STAGED_FALLBACK(h, buf + start[m], len[m], out + i * W);
         }
       }
@@ -499,6 +546,8 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   uint64_t* empty_bar = full_bar + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ __align__(16) ProtoSmem sp;
+  const u32 sa = stage_proto(proto, sp);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
@@ -579,7 +628,8 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   u32 used = 0;
   for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const u64 row_idx = tile * ROWS + t;
-    H h = proto;
+    H h;
+    init_state(h, proto, sa);
     bool fast = true;
     if constexpr (STREAM) {
       if (row_idx < n) {
@@ -689,6 +739,8 @@ __global__ void __launch_bounds__(32, MINB)
   const u64 my_tiles = g < ntiles ? (ntiles - g + G - 1) / G : 0;
   const u64 total = my_tiles * nst;
 
+  __shared__ __align__(16) ProtoSmem sp;
+  const u32 sa = stage_proto(proto, sp);
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
@@ -729,10 +781,10 @@ __global__ void __launch_bounds__(32, MINB)
         h.init(rec[m].h, half);
         fast = rec[m].tlen == 0;
       } else {
-        h.init(proto, half);
+        h.load_state(sa, proto, half);
       }
     } else {
-      h.init(proto, half);
+      h.load_state(sa, proto, half);
     }
   };
   u64 tile = g;

@@ -114,7 +114,7 @@ __global__ void k_sip_round_states(u64* __restrict__ states, u64 n, int rounds, 
        i += (u64)gridDim.x * blockDim.x) {
     u64 v0 = states[4 * i], v1 = states[4 * i + 1], v2 = states[4 * i + 2],
         v3 = states[4 * i + 3];
-    for (int r = 0; r < rounds; ++r) sip_round(v0, v1, v2, v3, k);
+    sip_rounds<0>(v0, v1, v2, v3, k, rounds);  // both round variants, alternating
     states[4 * i] = v0;
     states[4 * i + 1] = v1;
     states[4 * i + 2] = v2;
@@ -216,7 +216,7 @@ int lh_sip_round_states(uint64_t* d_states, uint64_t n, int rounds, void* stream
   if (rounds < 0 || (n && !d_states)) return LH_EINVAL;
   if ((uintptr_t)d_states % 8) return LH_EALIGN;
   if (!n || !rounds) return LH_OK;
-  const SipMul k = {1u, 1u << 13, 1u << 17, 1u << 21};
+  const SipMul k = {1u, 1u << 13, 1u << 17, 1u << 16};
   k_sip_round_states<<<grid_for(n, sm_count()), 256, 0, (cudaStream_t)stream>>>(d_states, n,
                                                                                 rounds, k);
   return cudaGetLastError() == cudaSuccess ? LH_OK : LH_ECUDA;

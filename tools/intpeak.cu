@@ -174,9 +174,7 @@ __global__ void __launch_bounds__(256) k_sipround(const SipMul km, u64* out, int
     for (int k = 0; k < 4; ++k) v[s][k] = (u64)(threadIdx.x + 1) * (k + 3 + s) + blockIdx.x;
   for (int i = 0; i < iters; i += 8) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-#pragma unroll
-      for (int s = 0; s < 2; ++s) sip_round(v[s][0], v[s][1], v[s][2], v[s][3], km);
+    for (int s = 0; s < 2; ++s) sip_rounds<8>(v[s][0], v[s][1], v[s][2], v[s][3], km, 8);
   }
   u64 x = 0;
 #pragma unroll
@@ -251,7 +249,7 @@ int main() {
   const int ublocks = sms * 2, uiters = 8192;  // 16 warps per SM, as the bench kernel
   float ms = time_ms([&] { k_update<<<ublocks, 256>>>(proto, (u64*)d, uiters); });
   const double updates = (double)ublocks * 256 * uiters / (ms * 1e-3);
-  const SipMul km{1u, 1u << 13, 1u << 17, 1u << 21};
+  const SipMul km{1u, 1u << 13, 1u << 17, 1u << 16};
   const int sblocks = sms * 8, siters = 4096;
   ms = time_ms([&] { k_sipround<<<sblocks, 256>>>(km, (u64*)d, siters); });
   const double sips = (double)sblocks * 256 * siters * 2 / (ms * 1e-3);
