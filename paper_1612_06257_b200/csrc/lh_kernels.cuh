@@ -405,7 +405,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
         const u64 i = base + 32 * m + lane;
         if (i < n) {
           Highway h;
+#ifdef LH_FALLBACK_PARAM_COPY  // A/B knob
+          h = proto;
+#else
           h.load_state(s_state_a, proto);
+#endif
           LH_STAGED_FALLBACK(h, buf + start[m], len[m], out + i * W);
         }
       }
@@ -507,11 +511,22 @@ __global__ void __launch_bounds__(WARPS * 32) k_staged_any(const H proto,
 // --------------------------------------------------------------------------
 // TMA-staged fixed-length kernel.
 // Requirements (checked on the host): len % 16 == 0, d_msgs 16-B aligned.
-// Shared ring: STAGES x [ROWS rows x 128 B] with the 128-byte swizzle:
-// 16-byte unit u of row t lives at t*128 + ((u ^ (t & 7)) << 4).
+// Shared ring: STAGES x [ROWS rows x BOX B].  BOX = 128 (the default) uses
+// the 128-byte swizzle: 16-byte unit u of row t lives at
+// t*128 + ((u ^ (t & 7)) << 4); BOX = 64 the 64-byte swizzle:
+// t*64 + ((u ^ ((t >> 1) & 3)) << 4).  Either way the 8 rows a quarter-warp
+// reads with LDS.128 hit distinct bank groups.  64-byte boxes halve the
+// bytes per stage, so an INT-bound hash (SipHash) gets twice the stages --
+// more slack between its fastest and slowest consumer warp -- in the same
+// shared memory.
 // --------------------------------------------------------------------------
 
 constexpr int kBoxBytes = 128;
+
+template <int BOX>
+__device__ __forceinline__ u32 swz_unit(u32 u, u32 t) {
+  return BOX == 128 ? (u ^ (t & 7)) : (u ^ ((t >> 1) & 3));
+}
 
 // Rows per TMA box (boxDim <= 256): ROWS itself, else the largest divisor
 // of ROWS that is a multiple of 32 and <= 256.
@@ -522,23 +537,25 @@ constexpr int tma_box_rows(int rows) {
   return 32;
 }
 
-template <int ROWS, int STAGES>
+template <int ROWS, int STAGES, int BOX = kBoxBytes>
 constexpr size_t tma_smem_bytes() {
-  return 1024 /*alignment slack*/ + (size_t)STAGES * ROWS * kBoxBytes + 2 * STAGES * 8;
+  return 1024 /*alignment slack*/ + (size_t)STAGES * ROWS * BOX + 2 * STAGES * 8;
 }
 
 // STREAM: the streaming append of whole-block chunks (lh_stream_update):
 // each row starts from its StreamRec's state instead of the prototype and
 // stores the state back instead of finishing; a row with a pending tail
 // (not block-aligned) takes the generic append from global memory.
-template <class H, int ROWS, int STAGES, int MINB, bool STREAM = false>
+template <class H, int ROWS, int STAGES, int MINB, bool STREAM = false, int BOX = kBoxBytes>
 __global__ void __launch_bounds__(ROWS + 32, MINB)
     k_tma_fixed(const __grid_constant__ CUtensorMap tmap, const H proto, u64 n, u64 len,
                 u64* __restrict__ out, u32 pf, StreamRec<H>* __restrict__ rec,
                 const uint8_t* __restrict__ chunks) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  constexpr u32 kStageBytes = ROWS * kBoxBytes;
+  static_assert(BOX == 128 || BOX == 64, "box width");
+  constexpr u32 kStageBytes = ROWS * BOX;
+  constexpr u32 kUnits = BOX / 16, kPkts = BOX / 32;  // 16-B units / packets per row-chunk
   constexpr int kConsumerWarps = ROWS / 32;
   constexpr int kBoxRowsTma = tma_box_rows(ROWS);  // TMA box rows <= 256
   constexpr int kBoxesPerStage = ROWS / kBoxRowsTma;
@@ -559,7 +576,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   __syncthreads();
 
   const u64 ntiles = (n + ROWS - 1) / ROWS;
-  const u32 nchunks = (u32)((len + kBoxBytes - 1) / kBoxBytes);
+  const u32 nchunks = (u32)((len + BOX - 1) / BOX);
 
   if (warp == kConsumerWarps) {
     // ---- producer: one elected lane streams boxes into the ring ----
@@ -571,7 +588,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
       u32 pf_c = 0;
       for (u32 k = 0; k < pf && pf_tile < ntiles; ++k) {
         for (int b = 0; b < kBoxesPerStage; ++b)
-          tma_prefetch_l2_2d(&tmap, (int32_t)(pf_c * kBoxBytes),
+          tma_prefetch_l2_2d(&tmap, (int32_t)(pf_c * BOX),
                              (int32_t)(pf_tile * ROWS + b * kBoxRowsTma));
         if (++pf_c == nchunks) { pf_c = 0; pf_tile += gridDim.x; }
       }
@@ -586,12 +603,12 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
           mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
 #pragma unroll
           for (int b = 0; b < kBoxesPerStage; ++b)
-            tma_load_2d(smem + s * kStageBytes + b * kBoxRowsTma * kBoxBytes, &tmap,
-                        (int32_t)(c * kBoxBytes), (int32_t)(tile * ROWS + b * kBoxRowsTma),
+            tma_load_2d(smem + s * kStageBytes + b * kBoxRowsTma * BOX, &tmap,
+                        (int32_t)(c * BOX), (int32_t)(tile * ROWS + b * kBoxRowsTma),
                         &full_bar[s]);
           if (pf && pf_tile < ntiles) {
             for (int b = 0; b < kBoxesPerStage; ++b)
-              tma_prefetch_l2_2d(&tmap, (int32_t)(pf_c * kBoxBytes),
+              tma_prefetch_l2_2d(&tmap, (int32_t)(pf_c * BOX),
                                  (int32_t)(pf_tile * ROWS + b * kBoxRowsTma));
             if (++pf_c == nchunks) { pf_c = 0; pf_tile += gridDim.x; }
           }
@@ -603,15 +620,14 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
 
   // ---- consumers: thread t owns message row tile*ROWS + t ----
   const u32 t = threadIdx.x;
-  const u32 sw = t & 7;
-  // Shared addresses of this thread's 8 swizzled 16-byte units in stage 0.
-  const u32 row0 = smem_u32(smem) + t * kBoxBytes;
+  // Shared addresses of this thread's swizzled 16-byte units in stage 0.
+  const u32 row0 = smem_u32(smem) + t * BOX;
   // Kept live in registers (opaque to ptxas, which would otherwise recompute
   // them per chunk); the stage offset is folded into LDS immediates below.
-  u32 ua[8];
+  u32 ua[kUnits];
 #pragma unroll
-  for (u32 u = 0; u < 8; ++u)
-    asm volatile("mov.b32 %0, %1;" : "=r"(ua[u]) : "r"(row0 + ((u ^ sw) << 4)));
+  for (u32 u = 0; u < kUnits; ++u)
+    asm volatile("mov.b32 %0, %1;" : "=r"(ua[u]) : "r"(row0 + (swz_unit<BOX>(u, t) << 4)));
   const int W = nout(proto);
   const u64 nfull = len >> 5;
   const u32 r = (u32)(len & 31);  // 0 or 16
@@ -622,7 +638,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
   // leaves the last slots of its final round unused).  Per chunk: one
   // wait, one compare, the arrive and a bit flip; the message epilogue is a
   // single copy outside the unrolled body (I-cache: the Sip bodies are big).
-  const u32 nfull4 = (u32)(nfull >> 2);  // chunks that hold 4 whole packets
+  const u32 nfull4 = (u32)(nfull / kPkts);  // chunks that hold kPkts whole packets
   u32 bars;  // shared address of full_bar[0]; empty_bar[s] = bars + 8 * (STAGES + s)
   asm volatile("mov.b32 %0, %1;" : "=r"(bars) : "r"(smem_u32(full_bar)));
   u32 used = 0;
@@ -647,7 +663,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
           used ^= 1u << ss;
           if (c < nfull4) {
 #pragma unroll
-            for (u32 k = 0; k < 4; ++k) {
+            for (u32 k = 0; k < kPkts; ++k) {
               const uint4 a = lds128(ua[2 * k] + ss * kStageBytes);
               const uint4 b = lds128(ua[2 * k + 1] + ss * kStageBytes);
               const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
@@ -655,17 +671,17 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
             }
           } else {
             // Last chunk of a message whose length is not a multiple of
-            // 128: 0..3 whole packets, then the 16-byte tail if r != 0.
-            const u32 kvalid = (u32)(nfull - 4ull * c);
+            // BOX: 0..kPkts-1 whole packets, then the 16-byte tail if r != 0.
+            const u32 kvalid = (u32)(nfull - (u64)kPkts * c);
             const u32 rowa = row0 + ss * kStageBytes;
             for (u32 k = 0; k < kvalid; ++k) {
-              const uint4 a = lds128(rowa + (((2 * k) ^ sw) << 4));
-              const uint4 b = lds128(rowa + (((2 * k + 1) ^ sw) << 4));
+              const uint4 a = lds128(rowa + (swz_unit<BOX>(2 * k, t) << 4));
+              const uint4 b = lds128(rowa + (swz_unit<BOX>(2 * k + 1, t) << 4));
               const u64 p[4] = {pack(a.x, a.y), pack(a.z, a.w), pack(b.x, b.y), pack(b.z, b.w)};
               if (!STREAM || fast) h.absorb32(p);
             }
             if (r) {
-              const uint4 a = lds128(rowa + (((2 * kvalid) ^ sw) << 4));
+              const uint4 a = lds128(rowa + (swz_unit<BOX>(2 * kvalid, t) << 4));
               tl[0] = pack(a.x, a.y);
               tl[1] = pack(a.z, a.w);
             }
@@ -1024,13 +1040,13 @@ int launch_staged_any(const H& proto, const uint8_t* buf, const u64* offsets, co
   return cuda_err(cudaGetLastError());
 }
 
-template <class H, int ROWS, int STAGES, int MINB, bool STREAM = false>
+template <class H, int ROWS, int STAGES, int MINB, bool STREAM = false, int BOX = kBoxBytes>
 int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out,
                    cudaStream_t st, int sms, StreamRec<H>* rec = nullptr) {
   auto enc = get_encode();
   if (!enc) return LH_ECUDA;
-  constexpr size_t smem = tma_smem_bytes<ROWS, STAGES>();
-  auto kern = k_tma_fixed<H, ROWS, STAGES, MINB, STREAM>;
+  constexpr size_t smem = tma_smem_bytes<ROWS, STAGES, BOX>();
+  auto kern = k_tma_fixed<H, ROWS, STAGES, MINB, STREAM, BOX>;
   int per_sm = 0;
   const int prc = prepare_kernel((const void*)kern, ROWS + 32, smem, &per_sm);
   if (prc) return prc;
@@ -1042,11 +1058,11 @@ int launch_tma_cfg(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)len, (cuuint64_t)nn};
     cuuint64_t strides[1] = {(cuuint64_t)len};
-    cuuint32_t box[2] = {(cuuint32_t)kBoxBytes, (cuuint32_t)tma_box_rows(ROWS)};
+    cuuint32_t box[2] = {(cuuint32_t)BOX, (cuuint32_t)tma_box_rows(ROWS)};
     cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)(msgs + base * len), dims,
                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      BOX == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return LH_ECUDA;
     const u64 tiles = (nn + ROWS - 1) / ROWS;
@@ -1119,6 +1135,12 @@ int tma_cfg_override() {
     if (!strcmp(s, "384x4")) return 5;
     if (!strcmp(s, "320x5")) return 6;
     if (!strcmp(s, "448x3")) return 7;
+    if (!strcmp(s, "512x6b64")) return 8;
+    if (!strcmp(s, "256x6b64")) return 9;
+    if (!strcmp(s, "512x5b64")) return 10;
+    if (!strcmp(s, "512x3b64m2")) return 11;
+    if (!strcmp(s, "480x3b64m2")) return 12;
+    if (!strcmp(s, "512x4b64")) return 13;
     return 0;
   }();
   return cfg;
@@ -1138,6 +1160,12 @@ int launch_tma(const H& proto, const uint8_t* msgs, u64 n, u64 len, u64* out, cu
     case 6: return launch_tma_cfg<H, 320, 5, 1>(proto, msgs, n, len, out, st, sms);
     case 7: return launch_tma_cfg<H, 448, 3, 1>(proto, msgs, n, len, out, st, sms);
     case 4: return launch_tma_cfg<H, 128, 3, 4>(proto, msgs, n, len, out, st, sms);
+    case 8: return launch_tma_cfg<H, 512, 6, 1, false, 64>(proto, msgs, n, len, out, st, sms);
+    case 9: return launch_tma_cfg<H, 256, 6, 2, false, 64>(proto, msgs, n, len, out, st, sms);
+    case 10: return launch_tma_cfg<H, 512, 5, 1, false, 64>(proto, msgs, n, len, out, st, sms);
+    case 11: return launch_tma_cfg<H, 512, 3, 2, false, 64>(proto, msgs, n, len, out, st, sms);
+    case 12: return launch_tma_cfg<H, 480, 3, 2, false, 64>(proto, msgs, n, len, out, st, sms);
+    case 13: return launch_tma_cfg<H, 512, 4, 1, false, 64>(proto, msgs, n, len, out, st, sms);
     default: break;
   }
   // One 512-row CTA per SM (16 consumer warps sharing a 3 x 64 KiB ring)
