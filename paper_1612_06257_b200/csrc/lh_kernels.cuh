@@ -404,11 +404,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       for (int m = 0; m < MPL; ++m) {
         const u64 i = base + 32 * m + lane;
         if (i < n) {
+          // A parameter copy here, not load_state: measured 1.78 vs 1.87 ms
+          // on cfg3 (the fallback's code shape moves the fast path's
+          // schedule).  Ring depth 2 here is parity-tested at rounds 0..5;
+          // the ptxas hazard of DESIGN.md §10 was seen at depth 1 only.
+#ifdef LH_FALLBACK_LOAD_STATE  // A/B knob
           Highway h;
-#ifdef LH_FALLBACK_PARAM_COPY  // A/B knob
-          h = proto;
-#else
           h.load_state(s_state_a, proto);
+#else
+          Highway h = proto;
 #endif
           LH_STAGED_FALLBACK(h, buf + start[m], len[m], out + i * W);
         }

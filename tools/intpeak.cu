@@ -182,6 +182,46 @@ __global__ void __launch_bounds__(256) k_sipround(const SipMul km, u64* out, int
   if (x == 0x12345678ull) out[0] = x;
 }
 
+// SipRound instruction-selection variants (A/B for csrc/lh_device.cuh):
+//  0 the engine's sip_rounds (W16 alternating)     1 rot16 by PRMT every round
+//  2 rot16 by IMAD.WIDE every round                3 as 0 with plain 64-bit adds
+//  4 no IMAD.WIDE (rot13/17 by SHF), mixed adds    5 as 4 with plain adds
+template <int V>
+__device__ __forceinline__ void sip_round_v(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k,
+                                            int r) {
+  auto add = [&](u64 a, u64 b) { return (V == 3 || V == 5) ? a + b : add64_mixed(a, b, k.one); };
+  const bool w16 = V == 2 || ((V == 0 || V == 3) && (r & 1));
+  v0 = add(v0, v1);
+  v1 = V >= 4 ? rotl_xor_shf<13>(v1, v0) : rotl_xor_wide(v1, k.m13, v0);
+  v0 = rot32(v0);
+  v2 = add(v2, v3);
+  v3 = w16 ? rotl_xor_wide(v3, k.m16, v2) : rotl16_xor_prmt(v3, v2);
+  v0 = add(v0, v3);
+  v3 = rotl_xor_shf<21>(v3, v0);
+  v2 = add(v2, v1);
+  v1 = V >= 4 ? rotl_xor_shf<17>(v1, v2) : rotl_xor_wide(v1, k.m17, v2);
+  v2 = rot32(v2);
+}
+
+template <int V, int S>
+__global__ void __launch_bounds__(256) k_sipvar(const SipMul km, u64* out, int iters) {
+  u64 v[S][4];
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[s][k] = (u64)(threadIdx.x + 1) * (k + 3 + s) + blockIdx.x;
+  for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int s = 0; s < S; ++s) sip_round_v<V>(v[s][0], v[s][1], v[s][2], v[s][3], km, j);
+  }
+  u64 x = 0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) x ^= v[s][0] ^ v[s][1] ^ v[s][2] ^ v[s][3];
+  if (x == 0x12345678ull) out[0] = x;
+}
+
 template <class F>
 static float time_ms(F f) {
   cudaEvent_t a, b;
@@ -254,6 +294,16 @@ int main() {
   ms = time_ms([&] { k_sipround<<<sblocks, 256>>>(km, (u64*)d, siters); });
   const double sips = (double)sblocks * 256 * siters * 2 / (ms * 1e-3);
   printf(" \"highway_update_per_s\": %.5e, \"sipround_per_s\": %.5e,\n", updates, sips);
+  printf(" \"sipround_variants_clk_per_warp_round\": {");
+#define RUN_SV(V, S, FIRST)                                                                     \
+  {                                                                                            \
+    const float m = time_ms([&] { k_sipvar<V, S><<<sblocks, 256>>>(km, (u64*)d, siters); });   \
+    const double r = (double)sblocks * 256 * siters * S / (m * 1e-3);                        \
+    printf("%s\"v%d_s%d\": %.4e", FIRST ? "" : ", ", V, S, r);                                  \
+  }
+  RUN_SV(0, 1, 1) RUN_SV(0, 2, 0) RUN_SV(1, 1, 0) RUN_SV(1, 2, 0) RUN_SV(2, 1, 0) RUN_SV(2, 2, 0)
+  RUN_SV(3, 1, 0) RUN_SV(3, 2, 0) RUN_SV(4, 1, 0) RUN_SV(4, 2, 0) RUN_SV(5, 1, 0) RUN_SV(5, 2, 0)
+  printf("},\n");
   printf(" \"status\": \"%s\"}\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
