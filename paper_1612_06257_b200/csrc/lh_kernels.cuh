@@ -422,204 +422,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
 }
 
 // --------------------------------------------------------------------------
-// Ragged short keys with the group's bytes and metadata prefetched one group
-// ahead by cp.async (LDGSTS: global -> shared without registers), so the
-// DRAM latency of staging overlaps the previous group's hashing instead of
-// stalling the warp (ncu on k_ragged_short: ~20% of warp stall samples sat
-// on the staging and metadata loads).  Per warp, a persistent loop over its
-// groups of G = 32 * MPL consecutive messages:
-//   wait for {span(j), meta(j+1)};  bounds of group j+1 from meta(j+1);
-//   issue {span(j+1), meta(j+2)};   hash group j from span(j), meta(j).
-// Shared memory per warp: 2 span buffers, 3 metadata buffers.  Hashing is
-// k_ragged_short's two non-divergent Update slots + finalization; groups
-// that fail the fast-path test (a message > 64 B, or outside the span
-// window) are hashed per lane from global memory with the ring reader.
-// Offsets/lengths are copied with 8- / 4-byte cp.async (natural alignment
-// is all the C ABI guarantees).
-// --------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async8(u32 dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(u32 dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(u32 dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
-// One short message (<= 64 B) from the stage: S = the staged words, a/sh =
-// its first 32-bit word and byte shift in the stage.  Slots as in
-// k_ragged_short.
-__device__ __forceinline__ void hash_short_staged(Highway& h, const u32* S, u32 a, u32 sh, u32 L,
-                                                  u64* out) {
-  auto word = [&](u32 k) { return __funnelshift_r(S[a + k], S[a + k + 1], sh); };
-  const u32 nfull = L >> 5, r = L & 31;
-  if (nfull) {
-    u32 P[8];
-#pragma unroll
-    for (u32 j = 0; j < 8; ++j) P[j] = word(j);
-    h.update(pack(P[0], P[1]), pack(P[2], P[3]), pack(P[4], P[5]), pack(P[6], P[7]));
-  }
-  if (r || nfull == 2) {
-    const u32 b = nfull ? 8u : 0u;
-    const u32 q = r ? (r >> 2) : 8u;
-    const u32 nleft = r ? (r & 3u) : 4u;
-    u32 P[8];
-#pragma unroll
-    for (u32 j = 0; j < 7; ++j) P[j] = j < q ? word(b + j) : 0u;
-    const u32 lft = word(b + (q < 7 ? q : 7u));
-    P[7] = lft & (nleft >= 4 ? 0xffffffffu : ((1u << (8 * nleft)) - 1u));
-    rem_tweak(h, r);
-    h.update(pack(P[0], P[1]), pack(P[2], P[3]), pack(P[4], P[5]), pack(P[6], P[7]));
-  }
-  h.finalize_out(out);
-}
-
-template <int WARPS, int MPL>
-__global__ void __launch_bounds__(WARPS * 32) k_ragged_pf(const Highway proto,
-                                                          const uint8_t* __restrict__ buf,
-                                                          const u64* __restrict__ offsets,
-                                                          const u32* __restrict__ lengths, u64 n,
-                                                          u64* __restrict__ out) {
-  constexpr u32 G = 32 * MPL;             // messages per group
-  constexpr u32 kSpan = kSpanCap * MPL;   // staged bytes per group (max)
-  constexpr u32 kSpanU4 = kSpan / 16 + 8;
-  __shared__ __align__(16) uint4 span[WARPS][2][kSpanU4];
-  __shared__ __align__(16) u64 moff[WARPS][3][G + 2];
-  __shared__ __align__(16) u32 mlen[WARPS][3][G];
-  __shared__ __align__(16) ProtoSmem sp;
-  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int W = proto.width / 64;
-  const u32 sa = stage_proto(proto, sp);
-  __syncthreads();
-  const u64 stride = (u64)gridDim.x * WARPS * G;
-  const u64 base0 = ((u64)blockIdx.x * WARPS + warp) * G;
-  const u64 noff = lengths ? n : n + 1;  // offsets entries
-  const u64 bb = (u64)(uintptr_t)buf;
-
-  // meta(j): offsets[base .. base+G] (+1 in the n+1 form) and lengths.
-  auto issue_meta = [&](u64 base, u32 slot) {
-    const u32 dst = smem_u32(&moff[warp][slot][0]);
-    for (u32 k = lane; k < G + 1; k += 32)
-      if (base + k < noff) cp_async8(dst + 8 * k, offsets + base + k);
-    if (lengths) {
-      const u32 dl = smem_u32(&mlen[warp][slot][0]);
-      for (u32 k = lane; k < G; k += 32)
-        if (base + k < n) cp_async4(dl + 4 * k, lengths + base + k);
-    }
-  };
-  auto msg_at = [&](u32 slot, u64 base, u32 k, u64& st, u32& ln) {
-    st = moff[warp][slot][k];
-    ln = lengths ? mlen[warp][slot][k] : (u32)(moff[warp][slot][k + 1] - st);
-    (void)base;
-  };
-  // Fast-path test of a group from its metadata; on success the 16-B
-  // aligned span [lo_al, lo_al + 16 * nch) relative to buf.
-  auto bounds = [&](u64 base, u32 slot, u64& lo_al, u32& nch) -> bool {
-    u64 s0 = 0;
-    u32 l0 = 0;
-    msg_at(slot, base, 0, s0, l0);
-    s0 = __shfl_sync(0xffffffffu, s0, 0);
-    bool fits = true;
-    u32 reach = 0;
-#pragma unroll
-    for (int m = 0; m < MPL; ++m) {
-      const u32 k = 32 * m + lane;
-      if (base + k < n) {
-        u64 st;
-        u32 ln;
-        msg_at(slot, base, k, st, ln);
-        fits &= ln <= 64 && st >= s0 && st + ln - s0 <= kSpan;
-        reach = max(reach, (u32)(st + ln - s0));
-      }
-    }
-    if (!__all_sync(0xffffffffu, fits)) return false;
-    const u32 spn = __reduce_max_sync(0xffffffffu, reach);
-    lo_al = ((bb + s0) & ~15ull) - bb;
-    nch = (u32)((((bb + s0 + spn + 15) & ~15ull) - bb - lo_al) >> 4);
-    return true;
-  };
-  auto issue_span = [&](u64 lo_al, u32 nch, u32 slot) {
-    const u32 dst = smem_u32(&span[warp][slot][0]);
-    const uint8_t* src = buf + lo_al;
-    for (u32 c = lane; c < nch; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
-  };
-
-  if (base0 >= n) return;
-  // Prologue: meta(0) now, then {span(0), meta(1)}.
-  issue_meta(base0, 0);
-  cp_async_commit();
-  cp_async_wait_all();
-  __syncwarp();
-  u64 lo_cur = 0;
-  u32 nch_cur = 0;
-  bool fast_cur = bounds(base0, 0, lo_cur, nch_cur);
-  if (fast_cur) issue_span(lo_cur, nch_cur, 0);
-  if (base0 + stride < n) issue_meta(base0 + stride, 1);
-  cp_async_commit();
-
-  u32 j = 0;
-  for (u64 base = base0; base < n; base += stride, ++j) {
-    const u32 ms = j % 3, ss = j & 1;
-    cp_async_wait_all();
-    __syncwarp();
-    // Next group: bounds from its metadata, then its span and the metadata
-    // of the group after it.
-    const u64 nb = base + stride;
-    u64 lo_next = 0;
-    u32 nch_next = 0;
-    bool fast_next = false;
-    if (nb < n) {
-      fast_next = bounds(nb, (j + 1) % 3, lo_next, nch_next);
-      if (fast_next) issue_span(lo_next, nch_next, ss ^ 1);
-      if (nb + stride < n) issue_meta(nb + stride, (j + 2) % 3);
-    }
-    cp_async_commit();
-    // This group.
-    if (fast_cur) {
-      const u32* S = reinterpret_cast<const u32*>(&span[warp][ss][0]);
-#pragma unroll 1
-      for (int m = 0; m < MPL; ++m) {
-        const u32 k = 32 * m + lane;
-        const u64 i = base + k;
-        if (i >= n) break;
-        u64 st;
-        u32 L;
-        msg_at(ms, base, k, st, L);
-        const u32 o = (u32)(st - lo_cur), a = o >> 2, sh = (o & 3) * 8;
-        Highway h;
-        h.load_state(sa, proto);
-        hash_short_staged(h, S, a, sh, L, out + i * W);
-      }
-    } else {
-#pragma unroll 1
-      for (int m = 0; m < MPL; ++m) {
-        const u32 k = 32 * m + lane;
-        const u64 i = base + k;
-        if (i < n) {
-          u64 st;
-          u32 L;
-          msg_at(ms, base, k, st, L);
-          Highway h = proto;
-          LH_STAGED_FALLBACK(h, buf + st, L, out + i * W);
-        }
-      }
-    }
-    __syncwarp();  // the stage and metadata slots are reused two groups on
-    fast_cur = fast_next;
-    lo_cur = lo_next;
-    nch_cur = nch_next;
-  }
-  cp_async_wait_all();
-}
-
-// --------------------------------------------------------------------------
 // The same warp staging for any hasher (the Sip family's short keys): the
 // window of 32 * MPL messages <= 64 B is staged once, then each lane hashes
 // its MPL messages one after another, reading 32-bit words from the stage
@@ -1205,45 +1007,12 @@ int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u3
 }
 
 // Warp-staged short-key kernel (HighwayHash only), ragged or fixed layout.
-// LH_SHORT_KERNEL=pf2|pf4: the cp.async-prefetching short-key kernel
-// (k_ragged_pf, MPL 2 or 4) for ragged batches; A/B knob, read once.
-int short_kernel_choice() {
-  static const int v = [] {
-    const char* s = getenv("LH_SHORT_KERNEL");
-    if (!s) return 0;
-    if (!strcmp(s, "pf2")) return 2;
-    if (!strcmp(s, "pf4")) return 4;
-    if (!strcmp(s, "pf2w4")) return 3;
-    return 0;
-  }();
-  return v;
-}
-
-template <int WARPS, int MPL, int PER_SM>
-int launch_ragged_pf(const Highway& proto, const uint8_t* buf, const u64* offsets,
-                     const u32* lengths, u64 n, u64* out, cudaStream_t st, int sms) {
-  const u64 groups = (n + 32 * MPL - 1) / (32 * MPL);
-  const u64 blocks = (groups + WARPS - 1) / WARPS;
-  const u64 cap = (u64)sms * PER_SM;
-  k_ragged_pf<WARPS, MPL><<<(unsigned)(blocks < cap ? blocks : cap), WARPS * 32, 0, st>>>(
-      proto, buf, offsets, lengths, n, out);
-  return cuda_err(cudaGetLastError());
-}
-
 int launch_staged(const Highway& proto, const uint8_t* buf, const u64* offsets,
                   const u32* lengths, u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
   int sms = 0;
   int rc = check_device(&sms);
   if (rc) return rc;
   if (n == 0) return LH_OK;
-  if (offsets) {
-    switch (short_kernel_choice()) {
-      case 2: return launch_ragged_pf<2, 2, 10>(proto, buf, offsets, lengths, n, out, st, sms);
-      case 3: return launch_ragged_pf<4, 2, 5>(proto, buf, offsets, lengths, n, out, st, sms);
-      case 4: return launch_ragged_pf<2, 4, 5>(proto, buf, offsets, lengths, n, out, st, sms);
-      default: break;
-    }
-  }
   // 2 warps per block of 4 messages per lane (cfg3: MPL 1 / 4 warps 1.900 ms,
   // MPL 2 1.859, MPL 4 1.805, MPL 4 / 2 warps 1.784, MPL 8 2.17).
   constexpr int kWarps = 2;
