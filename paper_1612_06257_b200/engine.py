@@ -719,6 +719,8 @@ class StreamBatch:
             nn = d_off.numel() - 1 if d_len is None else d_off.numel()
             if nn != self.n:
                 raise ValueError("one chunk per message expected")
+            if nn and not torch.cuda.is_current_stream_capturing():
+                _plan(d_off, d_len, nn, nn, d_buf.numel(), self.device)  # layout check
             bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
             rc = _lib.lib().lh_stream_update(self.alg, self.state.data_ptr(), self.n, bp,
                                              d_off.data_ptr(),

@@ -126,3 +126,14 @@ def test_plan_rejects_bad_arguments():
                             res.data_ptr(), None) == _lib.LH_EINVAL
     assert l.lh_ragged_plan(off.data_ptr() + 4, None, 3, 3, 100, res.data_ptr(), res.data_ptr(),
                             res.data_ptr(), None) == _lib.LH_EALIGN
+
+
+def test_stream_ragged_append_layout_rejected():
+    sb = engine.StreamBatch(engine.ALG_HIGHWAY, synth.key256(), 3)
+    buf = torch.zeros(100, dtype=torch.uint8, device=DEV)
+    bad = torch.tensor([0, 50, 40, 101], dtype=torch.int64, device=DEV)
+    with pytest.raises(ValueError, match="invalid ragged layout"):
+        sb.append(buf, bad)
+    ok = torch.tensor([0, 50, 60, 100], dtype=torch.int64, device=DEV)
+    sb.append(buf, ok)
+    assert sb.finish().shape == (3,)
