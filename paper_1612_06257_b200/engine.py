@@ -431,8 +431,48 @@ def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes
     return to_u64(out_host)
 
 
+def _ragged_fast(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out, kernel, check):
+    """The common launch-bound call -- contiguous CUDA tensors of the right
+    dtypes on the current device -- in one ctypes call (the general path's
+    conversions cost more than a small kernel).  None if not applicable."""
+    if not (isinstance(buf, torch.Tensor) and isinstance(offsets, torch.Tensor) and _CUDA_CHECKED
+            and buf.is_cuda and offsets.is_cuda and buf.dtype is torch.uint8
+            and offsets.dtype is torch.int64 and buf.is_contiguous() and offsets.is_contiguous()):
+        return None
+    idx = buf.get_device()
+    if idx != torch.cuda.current_device() or offsets.get_device() != idx:
+        return None
+    if lengths is not None and not (isinstance(lengths, torch.Tensor) and lengths.is_cuda
+                                    and lengths.dtype is torch.int32 and lengths.is_contiguous()
+                                    and lengths.get_device() == idx):
+        return None
+    if buf.dim() != 1 or offsets.dim() != 1 or kernel not in (KERNEL_AUTO, KERNEL_DIRECT,
+                                                               KERNEL_RING, KERNEL_STAGED):
+        return None
+    n = offsets.numel() - 1 if lengths is None else offsets.numel()
+    if n < 0 or (lengths is not None and lengths.numel() != n):
+        return None
+    device = buf.device
+    if out is None:
+        out = torch.empty(_out_shape(n, lanes), dtype=torch.int64, device=device)
+    elif (out.device != device or out.dtype is not torch.int64
+          or out.shape != _out_shape(n, lanes) or not out.is_contiguous()):
+        _check_out(out, n, lanes, device)
+    if n:
+        if check and not torch.cuda.is_current_stream_capturing():
+            _plan(offsets, lengths, n, n, buf.numel(), device)
+        bp = buf.data_ptr() if buf.numel() else offsets.data_ptr()
+        _launch_ragged(kind, key, bp, offsets.data_ptr(),
+                       None if lengths is None else lengths.data_ptr(), n, p1, p2, tree, out,
+                       device, _ragged_kernel(kind, kernel, buf.numel(), n))
+    return out
+
+
 def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
             kernel=KERNEL_AUTO, check=True):
+    r = _ragged_fast(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out, kernel, check)
+    if r is not None:
+        return r
     device = _require_cuda()
     _ragged_kernel(kind, kernel, 0, 0)  # validate before any work
     host = not (isinstance(buf, torch.Tensor) and buf.is_cuda)

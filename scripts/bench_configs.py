@@ -68,13 +68,38 @@ def _cpu(fn, nbytes, nmsgs, sample, seconds):
             "sample": f"{sample}; {passes} passes, {secs:.2f} s, oracle/lh_oracle.c"}
 
 
+def _graph_time(fn, per_graph=16, reps=10):
+    """Device time per call: per_graph calls captured in one CUDA graph and
+    replayed (no host launch overhead between kernels)."""
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up on a side stream, as torch.cuda.graph requires
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(per_graph):
+            fn()
+    return _time(g.replay, reps, 2) / per_graph
+
+
 def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, calls, verbose):
     ms = _time(fn, steps, warmup)
+    call_ms = None
+    if bound == "latency":
+        # Small batches: a Python call costs more than its kernel; the
+        # fractions use the device time of graph-replayed calls.
+        call_ms, ms = ms, _graph_time(fn)
     if calls is not None:  # kernel names: filled in after one profiler session (bench.py)
         calls.append((name, fn))
     pk = peak_gbs()
     hbm = alg_bytes / ms / 1e6
     r = {"workload": name, "ms": round(ms, 4),
+         **({"ms_per_python_call": round(call_ms, 4),
+             "ms_note": "ms = device time per call (16 calls captured in a CUDA graph, "
+                        "replayed); ms_per_python_call includes the host call"}
+            if call_ms is not None else {}),
          "GB_per_s": round(payload / ms / 1e6, 1) if payload else None,
          "msgs_per_s": round(nmsgs / ms * 1e3, 1),
          "roofline": {"bound": bound, "hbm_achieved_gbs": round(hbm, 1), "hbm_peak_gbs": pk,
