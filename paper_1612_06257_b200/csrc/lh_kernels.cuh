@@ -265,65 +265,6 @@ __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_
 }
 
 // --------------------------------------------------------------------------
-// Register-ring reader with the HighwayHash state split over a thread pair
-// (lh::HighwayHalf, as k_tma_split): for ragged batches of medium/long
-// messages too few to fill the GPU with one thread each (cfg2: 65,536
-// messages of 0..1023 bytes = 2,048 warps, ~14 per SM).  Both threads of a
-// pair read the full 32-byte packets through the same branch-free reader
-// (adjacent lanes load the same lines, so the warp's 16 messages cost 16
-// line lookups per load, as 16 single-thread messages would) and absorb
-// their half: half the Update work per thread, twice the warps.  Only the
-// finalization exchanges v0 words between the pair (shuffles), so every
-// lane of a warp runs it together: the loop is warp-uniform and lanes past
-// n hash an empty dummy.
-// --------------------------------------------------------------------------
-struct HalfAbsorb {
-  HighwayHalf& h;
-  __device__ __forceinline__ void absorb32(const u64 (&p)[4]) {
-    h.update(h.half ? p[2] : p[0], h.half ? p[3] : p[1]);
-  }
-};
-
-template <int D>
-__global__ void __launch_bounds__(128) k_ragged_pair(const Highway proto,
-                                                     const uint8_t* __restrict__ buf,
-                                                     const u64* __restrict__ offsets,
-                                                     const u32* __restrict__ lengths,
-                                                     u64 fixed_len, u64 n,
-                                                     u64* __restrict__ out) {
-  const int W = proto.width / 64;
-  __shared__ __align__(16) ProtoSmem sp;
-  const u32 sa = stage_proto(proto, sp);
-  __syncthreads();
-  const u32 lane = threadIdx.x & 31, half = lane & 1;
-  const u64 stride = (u64)gridDim.x * blockDim.x / 2;  // messages per grid pass
-  for (u64 base = ((u64)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) / 2; base < n;
-       base += stride) {
-    const u64 i = base + (lane >> 1);
-    const bool valid = i < n;
-    u64 off = 0, len = 0;
-    if (valid) {
-      if (offsets) {
-        off = offsets[i];
-        len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
-      } else {
-        off = i * fixed_len;
-        len = fixed_len;
-      }
-    }
-    HighwayHalf h;
-    h.load_state(sa, proto, half);
-    HalfAbsorb ab{h};
-    u64 t[4];
-    absorb_ring128<D>(ab, buf + off, len, t);
-    if (len & 31) h.remainder(t, (u32)(len & 31));
-    __syncwarp();
-    h.finalize_rounds();  // whole warp: v0 shuffles between the halves
-    if (valid) h.store(out + i * W);
-  }
-}
-
-// --------------------------------------------------------------------------
 // Ragged short-message kernel (cfg3: 2^26 keys of 8..64 bytes, finalization
 // dominated).  Each warp takes 32 consecutive messages.  Fast path (every
 // message <= 64 B and inside the kSpanCap-byte window that starts at lane
@@ -1043,16 +984,6 @@ static_assert(kRingDepth >= 2 && LH_FALLBACK_DEPTH >= 2,
               "ring depth 1 is not used (DESIGN.md §10)");
 #endif
 
-// Pair kernel for HighwayHash ring launches of fewer than LH_PAIR_MAX_PER_SM
-// messages per SM (env knob for A/B; 0 disables).
-bool ring_pair_choice(u64 n, int sms) {
-  static const long per_sm = [] {
-    const char* s = getenv("LH_PAIR_MAX_PER_SM");
-    return s ? atol(s) : 1024L;
-  }();
-  return per_sm > 0 && n < (u64)sms * (u64)per_sm;
-}
-
 template <class H>
 int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths,
                 u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
@@ -1066,16 +997,9 @@ int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u3
   // Ring depth: 2 for HighwayHash (equal or better than 4 everywhere), 4 for
   // Sip (short keys need it: cfg3-shaped SipHash-2-4 2.85 ms vs 3.09).
   const unsigned grid = grid_for(n, 128, sms);
-  if constexpr (std::is_same<H, Highway>::value) {
-    if (ring_pair_choice(n, sms)) {
-      const unsigned g2 = grid_for(2 * n, 128, sms);
-      k_ragged_pair<kRingDepth><<<g2, 128, 0, st>>>(proto, buf, offsets, lengths, fixed_len, n,
-                                                     out);
-    } else {
-      k_ragged_ring<H, kRingDepth, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
-                                                               fixed_len, n, out);
-    }
-  }
+  if constexpr (std::is_same<H, Highway>::value)
+    k_ragged_ring<H, kRingDepth, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
+                                                             fixed_len, n, out);
   else
     k_ragged_ring<H, 4, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths, fixed_len, n,
                                                     out);
