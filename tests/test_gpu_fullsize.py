@@ -71,6 +71,41 @@ def test_cfg3_short_keys_2p26(oracle):
     _log("cfg3 hh64 2^26 ragged", n, t0)
 
 
+def test_cfg3_shaped_sip_and_wide_2p26(oracle):
+    """The cfg3 layout under every other hash the bench times on it
+    (SipHash-2-4 / -1-3, staged kernel) and HighwayHash-256: every digest."""
+    n = 1 << 26
+    lens = torch.empty(n, dtype=torch.int32, device=DEV)
+    synth.lengths_device(lens, 3, 8, 64)
+    off = torch.zeros(n, dtype=torch.int64, device=DEV)
+    off[1:] = torch.cumsum(lens[:-1].to(torch.int64), 0)
+    total = int(off[-1]) + int(lens[-1])
+    buf = _fill(total, 4)
+    hb, ho, hl = _host(buf), _host(off).view(np.uint64), _host(lens).view(np.uint32)
+    for name, alg, c, d in (("sip24", oracle.ALG_SIPHASH, 2, 4), ("sip13", oracle.ALG_SIPHASH, 1, 3)):
+        h = to_u64(engine.sip_ragged(synth.key128(), buf, off, lens, c, d))
+        t0 = time.perf_counter()
+        _mismatches(h, oracle.batch_ragged(alg, synth.key128(), hb, ho, hl, c, d), name)
+        _log(f"cfg3-shaped {name} 2^26 ragged", n, t0)
+    h = to_u64(engine.highway_ragged(synth.key256(), buf, off, lens, 256))
+    t0 = time.perf_counter()
+    _mismatches(h, oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), hb, ho, hl, 256, 4),
+                "hh256")
+    _log("cfg3-shaped hh256 2^26 ragged", n, t0)
+
+
+def test_cfg5_wide_digests_2p24(oracle):
+    """HighwayHash-128 / -256 over the 16 GiB cfg5 batch: every digest."""
+    n, L = 1 << 24, 1024
+    m = _fill(n * L, 6).view(n, L)
+    host = _host(m)
+    want = oracle.batch_fixed(oracle.ALG_HIGHWAY, synth.key256(), host, 256, 4)
+    t0 = time.perf_counter()
+    _mismatches(to_u64(engine.highway_batch(synth.key256(), m, 256)), want, "hh256")
+    _mismatches(to_u64(engine.highway_batch(synth.key256(), m, 128)), want[:, :2], "hh128")
+    _log("cfg5 hh128 + hh256 2^24 x 1 KiB", 2 * n, t0)
+
+
 def test_cfg4_long_messages_16GiB(oracle, golden):
     n, L = 16384, 1 << 20
     buf = _fill(n * L, 5)
