@@ -494,6 +494,7 @@ def run_ours(args):
         roof["t_roof_ms"] = round(max(t_hbm, ir["t_int_balanced_ms"]), 4)
         roof["frac_of_max_read_ceiling_or_int"] = round(roof["t_roof_ms"] / per_launch_ms, 4)
 
+    gather = gather_digests_timed(plane, out, dev) if ws > 1 else None
     e2e = run_e2e(args, plane, key, dev, start, n)
     result = None
     if rank == 0:
@@ -518,6 +519,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "checksum": [f"{x:016x}" for x in folds],
             "e2e": e2e,
+            **({"gather": gather} if gather else {}),
         }
     if args.scaling == "strong":
         strong = strong_cfg4(args, plane, key, dev)
@@ -575,6 +577,32 @@ def cpu_baseline_headline(min_seconds: float):
             "single_core": {"value": round(g1, 3), "unit": UNIT,
                             "sample": f"{p1} passes x {len(one)} msgs, 1 thread, {s1:.2f} s"},
             "host": _host_info()}
+
+
+def gather_digests_timed(plane: Plane, out, dev):
+    """SURVEY §8e's end-of-run exchange, outside the timed region: every
+    rank's digest slice all-gathered into one (n_total,) tensor on every
+    device (shard.gather_digests: NCCL all-gather over NVLink), timed on the
+    device with CUDA events, max over ranks."""
+    import torch
+
+    from paper_1612_06257_b200 import shard
+
+    n_total = int(plane.sum(out.shape[0]))
+    shard.gather_digests(out, n_total)  # warm-up (communicator setup)
+    torch.cuda.synchronize()
+    plane.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    full = shard.gather_digests(out, n_total)
+    b.record()
+    torch.cuda.synchronize()
+    ms = plane.max(a.elapsed_time(b))
+    nbytes = full.numel() * full.element_size()
+    del full
+    return {"what": "all-gather of every rank's digests to every rank (shard.gather_digests)",
+            "bytes_per_rank_out": nbytes, "ms": round(ms, 4),
+            "GB_per_s_per_rank": round(nbytes / ms / 1e6, 1)}
 
 
 def run_e2e(args, plane: Plane, key, dev, start: int, n_rank: int):
