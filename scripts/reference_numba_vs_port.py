@@ -98,7 +98,19 @@ def main():
         portN = orc.batch_fixed(oalg, k, msgs, op1, op2, nthreads=threads)
         t_portN = time.perf_counter() - t0
         assert np.array_equal(refN, portN), name
+        extra = {}
+        if algo == 0:  # the reference's numpy backend (S/_highway_np.py:116-130), 1 core
+            from lanehash import _highway_np
+            from lanehash.highway import Key256
+
+            k256 = Key256([int(x) for x in key])
+            t0 = time.perf_counter()
+            npd = _highway_np.hash64_batch(k256, one)
+            extra["numpy_backend_1core_GBps"] = round(one.nbytes / (time.perf_counter() - t0) / 1e9,
+                                                      3)
+            assert np.array_equal(npd, port1), name
         res[name] = {
+            **extra,
             "numba_1core_GBps": round(one.nbytes / t_ref1 / 1e9, 3),
             "port_1thread_GBps": round(one.nbytes / t_port1 / 1e9, 3),
             "numba_pool_GBps": round(msgs.nbytes / t_refN / 1e9, 3),
