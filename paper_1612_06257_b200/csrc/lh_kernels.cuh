@@ -663,11 +663,7 @@ __global__ void __launch_bounds__(ROWS + 32, MINB)
       for (u32 ss = 0; ss < (u32)STAGES; ++ss) {
         const u32 c = cb + ss;
         if (c < nchunks) {
-#ifdef LH_MBAR_HINT_NS  // A/B knob: suspend-time hint on the consumers' waits
-          mbar_wait_sleep(bars + 8 * ss, (used >> ss) & 1, LH_MBAR_HINT_NS);
-#else
           mbar_wait_addr(bars + 8 * ss, (used >> ss) & 1);
-#endif
           used ^= 1u << ss;
           if (c < nfull4) {
 #pragma unroll

@@ -59,24 +59,6 @@ __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-// As mbar_wait_addr, with a suspend-time hint: a warp whose phase is not
-// complete is suspended by the hardware (up to `ns` nanoseconds, woken when
-// the phase completes) instead of re-polling, so waiting consumer warps
-// stop taking issue slots from the warps that are hashing.
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(bar),
-      "r"(parity), "r"(ns)
-      : "memory");
-}
-
 __device__ __forceinline__ void mbar_arrive_addr(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
