@@ -5,6 +5,7 @@ per-rank checksum gather -- the same code the NCCL run uses."""
 import json
 import os
 
+import numpy as np
 import pytest
 
 import bench
@@ -60,3 +61,20 @@ def test_gpus_must_match_torchrun_world(monkeypatch):
 def test_config_identical_across_arms():
     assert bench.config_dict(1, "weak", bench.N_MSGS)["workload"].startswith("hh64_2^24x1KiB")
     assert bench.config_dict(2, "strong", 1 << 23)["global_messages"] == bench.N_MSGS
+
+
+def test_reference_arm_on_cpu(capsys):
+    """--impl reference runs the CPU implementation only (no GPU): one JSON
+    line with the contract's keys and the same config dict as our arm."""
+    assert bench.main(["--impl", "reference", "--steps", "1", "--warmup", "3",
+                       "--msgs", "4096"]) == 0
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["steps"] == 1
+    assert line["config"] == bench.config_dict(1, "weak", 4096)
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    from oracle import oracle as orc
+    from paper_1612_06257_b200 import synth
+
+    msgs = orc.synth_fill(4096 * 1024, bench.DATA_SEED).reshape(4096, 1024)
+    fold = np.bitwise_xor.reduce(orc.batch_fixed(orc.ALG_HIGHWAY, synth.key256(), msgs, 64, 4))
+    assert line["checksum"] == f"{int(fold):016x}"
