@@ -281,6 +281,21 @@ __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_
 // --------------------------------------------------------------------------
 constexpr u32 kSpanCap = 2048;  // bytes of a warp's span staged in smem
 
+// Shared-memory bounds checks for the staged kernels, compiled in only for
+// the A/B build LH_NVCC_EXTRA=-DLH_DEBUG_BOUNDS (compute-sanitizer is not
+// available on the GPU pool): an out-of-range stage index traps the kernel,
+// which the random-layout parity tests then report as a CUDA error.
+#ifdef LH_DEBUG_BOUNDS
+#define LH_CHECK(cond) \
+  do {                 \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define LH_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 // Length injection of UpdateRemainder (S/highway.py:188-197); r = 0 is a no-op.
 __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
 #pragma unroll
@@ -359,6 +374,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       const u64 lo_al = ((bb + lo) & ~15ull) - bb, hi_al = ((bb + hi + 15) & ~15ull) - bb;
       const u32 nch = (u32)((hi_al - lo_al) >> 4);
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
+      LH_CHECK(nch <= kSpan / 16 + 8);
       for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
       __syncwarp();
 #pragma unroll 1
@@ -369,7 +385,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
         const u32 L = (u32)len[m];
         const u32 nfull = L >> 5, r = L & 31;
         // Word k of the message (LE; bytes past L belong to other messages).
-        auto word = [&](u32 k) { return __funnelshift_r(S[a + k], S[a + k + 1], sh); };
+        auto word = [&](u32 k) {
+          LH_CHECK(a + k + 1 < (kSpan / 16 + 8) * 4);
+          return __funnelshift_r(S[a + k], S[a + k + 1], sh);
+        };
         Highway h;
         h.load_state(s_state_a, proto);
         // Slot 0: block 0 if the message has one (32..64 bytes); no tweak.
@@ -473,6 +492,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_staged_any(const H proto,
       const u64 lo_al = ((bb + s0) & ~15ull) - bb, hi_al = ((bb + s0 + span + 15) & ~15ull) - bb;
       const u32 nch = (u32)((hi_al - lo_al) >> 4);
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
+      LH_CHECK(nch <= kSpan / 16 + 8);
       for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
       __syncwarp();
 #pragma unroll 1
@@ -481,7 +501,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_staged_any(const H proto,
         if (i >= n) break;
         const u32 o = (u32)(start[m] - lo_al), a = o >> 2, sh = (o & 3) * 8;
         const u32 L = (u32)len[m];
-        auto word = [&](u32 k) { return __funnelshift_r(S[a + k], S[a + k + 1], sh); };
+        auto word = [&](u32 k) {
+          LH_CHECK(a + k + 1 < (kSpan / 16 + 8) * 4);
+          return __funnelshift_r(S[a + k], S[a + k + 1], sh);
+        };
         H h = proto;
         const u32 nb = L >> 5, r = L & 31;
         for (u32 b = 0; b < nb; ++b) {
