@@ -449,28 +449,25 @@ struct IsSipHash<Sip<C, D>> {
   static constexpr bool value = true;
 };
 
-#ifndef LH_SIP_SORT
-#define LH_SIP_SORT 1  // A/B knob: length-class sort of the staged SipHash group
-#endif
-
 // SipHash-c-d of a staged group of 32 * MPL short keys (<= 64 B), for
 // k_staged_any.  SipHash's cost grows with every 8-byte word and the warp
 // runs each round of its lanes until the round's longest key is done, so:
 //  * one flat loop over a key's whole words, then its final word -- at
 //    most 9 compressions per round (8 whole words + the length word)
 //    instead of absorb32 blocks plus tail words (up to 12);
-//  * (LH_SIP_SORT, ragged groups spanning more than one class) the group's
-//    keys are first ranked by length class (len >> 4: 0-15, 16-31, 32-47,
+//  * (SORT: ragged launches) the group's keys are first ranked by length class (len >> 4: 0-15, 16-31, 32-47,
 //    48-63, 64 bytes; invalid slots last) with warp ballots and re-dealt to
 //    the rounds through shared memory, so each round's lanes hash keys of
 //    similar length.  cfg3-shaped SipHash-2-4 2.45 -> 2.19 ms (flat loop)
-//    -> 2.00 ms (sorted).
+//    -> 2.00 ms (sorted).  Fixed rows (one length) keep the flat loop: the
+//    sort costs them ~13% (and a runtime "one class?" test moved the
+//    schedule enough to lose most of the ragged gain: a template flag).
 // Digest of key `base + slot` goes to out[base + slot] as before.
-template <int WARPS, int MPL, int C, int D>
+template <int WARPS, int MPL, bool SORT, int C, int D>
 __device__ __forceinline__ void hash_sip_group(const Sip<C, D>& proto, const u32* S,
                                                const u64 (&start)[MPL], const u64 (&len)[MPL],
                                                u64 base, u64 n, u64 lo_al, u32 lane, u32 warp,
-                                               bool ragged, u64* __restrict__ out) {
+                                               u64* __restrict__ out) {
   constexpr u32 G = 32 * MPL;
   auto hash_one = [&](u64 st, u32 L, u64 i) {
     const u32 o = (u32)(st - lo_al), a = o >> 2, sh = (o & 3) * 8;
@@ -482,63 +479,49 @@ __device__ __forceinline__ void hash_sip_group(const Sip<C, D>& proto, const u32
     if (tb) last = pack(word(2 * nw), word(2 * nw + 1)) & ((1ull << (8 * tb)) - 1);
     out[i] = v.final(last | ((u64)(L & 0xFF) << 56), proto.c, proto.d, proto.k);
   };
-#if LH_SIP_SORT
-  __shared__ u64 s_start[WARPS][G];
-  __shared__ u32 s_len[WARPS][G];
-  __shared__ uint16_t s_slot[WARPS][G];
-  u32 cls[MPL], lo = 5, hi = 0;
+  if constexpr (SORT) {
+    __shared__ u64 s_start[WARPS][G];
+    __shared__ u32 s_len[WARPS][G];
+    __shared__ uint16_t s_slot[WARPS][G];
+    u32 cls[MPL];
 #pragma unroll
-  for (int m = 0; m < MPL; ++m) {
-    const u32 L = (u32)len[m];
-    cls[m] = base + 32 * m + lane < n ? min(L >> 4, 4u) : 5u;
-    lo = min(lo, cls[m]);
-    hi = max(hi, cls[m] < 5u ? cls[m] : 0u);
-  }
-  // Fixed rows, or a ragged group of one class: nothing to gain (A/B: the
-  // sort costs ~13% on fixed 31-byte rows).
-  const bool sort = ragged && __reduce_min_sync(0xffffffffu, lo) != __reduce_max_sync(0xffffffffu, hi);
-  if (!sort) {
+    for (int m = 0; m < MPL; ++m) {
+      const u32 L = (u32)len[m];
+      cls[m] = base + 32 * m + lane < n ? min(L >> 4, 4u) : 5u;
+    }
+    const u32 lt = (1u << lane) - 1u;
+    u32 pos[MPL], next = 0;
+#pragma unroll
+    for (u32 c = 0; c < 6; ++c) {
+#pragma unroll
+      for (int m = 0; m < MPL; ++m) {
+        const u32 b = __ballot_sync(0xffffffffu, cls[m] == c);
+        if (cls[m] == c) pos[m] = next + __popc(b & lt);
+        next += __popc(b);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MPL; ++m) {
+      s_start[warp][pos[m]] = start[m];
+      s_len[warp][pos[m]] = (u32)len[m];
+      s_slot[warp][pos[m]] = (uint16_t)(32 * m + lane);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int m = 0; m < MPL; ++m) {
+      const u32 p = 32 * m + lane;
+      const u64 i = base + s_slot[warp][p];
+      if (i < n) hash_one(s_start[warp][p], s_len[warp][p], i);
+    }
+  } else {
+    (void)warp;
 #pragma unroll 1
     for (int m = 0; m < MPL; ++m) {
       const u64 i = base + 32 * m + lane;
       if (i >= n) break;
       hash_one(start[m], (u32)len[m], i);
     }
-    return;
   }
-  const u32 lt = (1u << lane) - 1u;
-  u32 pos[MPL], next = 0;
-#pragma unroll
-  for (u32 c = 0; c < 6; ++c) {
-#pragma unroll
-    for (int m = 0; m < MPL; ++m) {
-      const u32 b = __ballot_sync(0xffffffffu, cls[m] == c);
-      if (cls[m] == c) pos[m] = next + __popc(b & lt);
-      next += __popc(b);
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < MPL; ++m) {
-    s_start[warp][pos[m]] = start[m];
-    s_len[warp][pos[m]] = (u32)len[m];
-    s_slot[warp][pos[m]] = (uint16_t)(32 * m + lane);
-  }
-  __syncwarp();
-#pragma unroll 1
-  for (int m = 0; m < MPL; ++m) {
-    const u32 p = 32 * m + lane;
-    const u64 i = base + s_slot[warp][p];
-    if (i < n) hash_one(s_start[warp][p], s_len[warp][p], i);
-  }
-#else
-  (void)ragged, (void)warp;
-#pragma unroll 1
-  for (int m = 0; m < MPL; ++m) {
-    const u64 i = base + 32 * m + lane;
-    if (i >= n) break;
-    hash_one(start[m], (u32)len[m], i);
-  }
-#endif
 }
 
 // --------------------------------------------------------------------------
@@ -549,7 +532,7 @@ __device__ __forceinline__ void hash_sip_group(const Sip<C, D>& proto, const u32
 // keys per lane also evens out the per-lane work: SipHash's cost grows with
 // every 8-byte word, so lanes of one key each wait for the warp's longest.
 // --------------------------------------------------------------------------
-template <class H, int WARPS, int MPL>
+template <class H, int WARPS, int MPL, bool SORT = false>
 __global__ void __launch_bounds__(WARPS * 32) k_staged_any(const H proto,
                                                            const uint8_t* __restrict__ buf,
                                                            const u64* __restrict__ offsets,
@@ -597,8 +580,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_staged_any(const H proto,
       for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
       if constexpr (IsSipHash<H>::value) {
         __syncwarp();
-        hash_sip_group<WARPS, MPL>(proto, S, start, len, base, n, lo_al, lane, warp,
-                                   offsets != nullptr, out);
+        hash_sip_group<WARPS, MPL, SORT>(proto, S, start, len, base, n, lo_al, lane, warp, out);
         __syncwarp();
         continue;
       }
@@ -1170,8 +1152,14 @@ int launch_staged_any(const H& proto, const uint8_t* buf, const u64* offsets, co
   const u64 warps = (n + 32 * kMpl - 1) / (32 * kMpl);
   const u64 cap = (u64)sms * 256;
   const u64 blocks = (warps + kWarps - 1) / kWarps;
-  k_staged_any<H, kWarps, kMpl><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0, st>>>(
-      proto, buf, offsets, lengths, fixed_len, n, out);
+  const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
+  if (offsets && IsSipHash<H>::value)  // ragged SipHash: length-sorted rounds
+    k_staged_any<H, kWarps, kMpl, true><<<grid, kWarps * 32, 0, st>>>(proto, buf, offsets,
+                                                                        lengths, fixed_len, n,
+                                                                        out);
+  else
+    k_staged_any<H, kWarps, kMpl><<<grid, kWarps * 32, 0, st>>>(proto, buf, offsets, lengths,
+                                                                fixed_len, n, out);
   return cuda_err(cudaGetLastError());
 }
 
