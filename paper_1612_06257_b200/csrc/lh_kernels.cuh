@@ -321,7 +321,7 @@ __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
 #endif
 // MPL messages per lane per warp iteration (a group of 32 * MPL consecutive
 // messages staged together, hashed one after another by each lane).
-template <int WARPS, int MPL = LH_SHORT_MPL, bool SORT = false>
+template <int WARPS, int MPL = LH_SHORT_MPL>
 __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto,
                                                              const uint8_t* __restrict__ buf,
                                                              const u64* __restrict__ offsets,
@@ -376,53 +376,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
       LH_CHECK(nch <= kSpan / 16 + 8);
       for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
-      // SORT (ragged launches, A/B knob): deal the keys without a 32-byte
-      // block (L < 32) to the first rounds, so a round in which no lane has
-      // one skips slot 0 altogether (ballot ranking, through shared memory).
-      __shared__ u64 s_start[SORT ? WARPS : 1][SORT ? 32 * MPL : 1];
-      __shared__ u32 s_len[SORT ? WARPS : 1][SORT ? 32 * MPL : 1];
-      __shared__ uint16_t s_slot[SORT ? WARPS : 1][SORT ? 32 * MPL : 1];
-      if constexpr (SORT) {
-        u32 cls[MPL];
-#pragma unroll
-        for (int m = 0; m < MPL; ++m)
-          cls[m] = base + 32 * m + lane < n ? (len[m] >= 32 ? 1u : 0u) : 2u;
-        const u32 lt = (1u << lane) - 1u;
-        u32 pos[MPL], next = 0;
-#pragma unroll
-        for (u32 c = 0; c < 3; ++c) {
-#pragma unroll
-          for (int m = 0; m < MPL; ++m) {
-            const u32 bal = __ballot_sync(0xffffffffu, cls[m] == c);
-            if (cls[m] == c) pos[m] = next + __popc(bal & lt);
-            next += __popc(bal);
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < MPL; ++m) {
-          s_start[warp][pos[m]] = start[m];
-          s_len[warp][pos[m]] = (u32)len[m];
-          s_slot[warp][pos[m]] = (uint16_t)(32 * m + lane);
-        }
-      }
       __syncwarp();
 #pragma unroll 1
       for (int m = 0; m < MPL; ++m) {
-        u64 i, st;
-        u32 L;
-        if constexpr (SORT) {
-          const u32 p = 32 * m + lane;
-          i = base + s_slot[warp][p];
-          if (i >= n) continue;
-          st = s_start[warp][p];
-          L = s_len[warp][p];
-        } else {
-          i = base + 32 * m + lane;
-          if (i >= n) break;
-          st = start[m];
-          L = (u32)len[m];
-        }
-        const u32 o = (u32)(st - lo_al), a = o >> 2, sh = (o & 3) * 8;
+        const u64 i = base + 32 * m + lane;
+        if (i >= n) break;
+        const u32 o = (u32)(start[m] - lo_al), a = o >> 2, sh = (o & 3) * 8;
+        const u32 L = (u32)len[m];
         const u32 nfull = L >> 5, r = L & 31;
         // Word k of the message (LE; bytes past L belong to other messages).
         auto word = [&](u32 k) {
@@ -1159,16 +1119,6 @@ int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u3
   return cuda_err(cudaGetLastError());
 }
 
-// LH_SHORT_SORT=1: the slot-class sort in k_ragged_short's ragged launches
-// (A/B knob, read once).
-bool short_sort_enabled() {
-  static const bool v = [] {
-    const char* s = getenv("LH_SHORT_SORT");
-    return s && atoi(s) != 0;
-  }();
-  return v;
-}
-
 // Warp-staged short-key kernel (HighwayHash only), ragged or fixed layout.
 int launch_staged(const Highway& proto, const uint8_t* buf, const u64* offsets,
                   const u32* lengths, u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
@@ -1182,13 +1132,8 @@ int launch_staged(const Highway& proto, const uint8_t* buf, const u64* offsets,
   const u64 warps = (n + 32 * LH_SHORT_MPL - 1) / (32 * LH_SHORT_MPL);
   const u64 cap = (u64)sms * 8 * (64 / kWarps);
   const u64 blocks = (warps + kWarps - 1) / kWarps;
-  const unsigned grid = (unsigned)(blocks < cap ? blocks : cap);
-  if (offsets && short_sort_enabled())
-    k_ragged_short<kWarps, LH_SHORT_MPL, true><<<grid, kWarps * 32, 0, st>>>(
-        proto, buf, offsets, lengths, fixed_len, n, out);
-  else
-    k_ragged_short<kWarps><<<grid, kWarps * 32, 0, st>>>(proto, buf, offsets, lengths, fixed_len,
-                                                         n, out);
+  k_ragged_short<kWarps><<<(unsigned)(blocks < cap ? blocks : cap), kWarps * 32, 0, st>>>(
+      proto, buf, offsets, lengths, fixed_len, n, out);
   return cuda_err(cudaGetLastError());
 }
 
