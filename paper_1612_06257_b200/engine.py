@@ -181,14 +181,29 @@ def _out_shape(n: int, lanes: int):
     return (n,) if lanes == 1 else (n, lanes)
 
 
+_PEER_OK: dict = {}
+
+
+def _peer_ok(device, other) -> bool:
+    """Can kernels on `device` store to memory on `other` (NVLink / P2P)?"""
+    key = (device.index, other.index)
+    v = _PEER_OK.get(key)
+    if v is None:
+        v = _PEER_OK[key] = bool(torch.cuda.can_device_access_peer(device.index, other.index))
+    return v
+
+
 def _check_out(out: torch.Tensor, n: int, lanes: int, device) -> torch.Tensor:
     """A caller-supplied digest tensor must be exactly what the kernels write:
-    n * lanes contiguous 64-bit words on the launch device (else the launch
-    would write out of bounds or scramble digests)."""
+    n * lanes contiguous 64-bit words, on the launch device or on a GPU the
+    launch device can store to directly (peer access: the digests then go
+    straight into that GPU's memory, see peer.py); else the launch would
+    write out of bounds or scramble digests."""
     if not isinstance(out, torch.Tensor):
         raise ValueError("out must be a torch tensor")
-    if not out.is_cuda or out.device != device:
-        raise ValueError(f"out must be a CUDA tensor on {device}, got {out.device}")
+    if not out.is_cuda or (out.device != device and not _peer_ok(device, out.device)):
+        raise ValueError(f"out must be a CUDA tensor on {device} (or a peer-accessible "
+                         f"GPU), got {out.device}")
     if out.dtype not in (torch.int64, torch.uint64):
         raise ValueError(f"out must be int64 (or uint64), got {out.dtype}")
     if tuple(out.shape) != _out_shape(n, lanes) or not out.is_contiguous():
