@@ -494,7 +494,10 @@ def run_ours(args):
         roof["t_roof_ms"] = round(max(t_hbm, ir["t_int_balanced_ms"]), 4)
         roof["frac_of_max_read_ceiling_or_int"] = round(roof["t_roof_ms"] / per_launch_ms, 4)
 
-    gather = gather_digests_timed(plane, out, dev) if ws > 1 else None
+    gather = None
+    if ws > 1:
+        gather = gather_digests_timed(plane, out, dev)
+        gather["peer_stores"] = peer_store_steps(args, plane, key, msgs, start, n, stream)
     e2e = run_e2e(args, plane, key, dev, start, n)
     result = None
     if rank == 0:
@@ -603,6 +606,29 @@ def gather_digests_timed(plane: Plane, out, dev):
     return {"what": "all-gather of every rank's digests to every rank (shard.gather_digests)",
             "bytes_per_rank_out": nbytes, "ms": round(ms, 4),
             "GB_per_s_per_rank": round(nbytes / ms / 1e6, 1)}
+
+
+def peer_store_steps(args, plane: Plane, key, msgs, start: int, n: int, stream):
+    """The same step with the gather fused in (peer.py): every rank's kernel
+    stores its digests straight into rank 0's buffer (CUDA IPC, NVLink).
+    Max-over-ranks ms per step, to compare with ms_per_step + the NCCL
+    all-gather above."""
+    import torch
+
+    from paper_1612_06257_b200 import engine, peer
+
+    n_total = int(plane.sum(n))
+    buf = peer.shared_digest_buffer(n_total, 1, root=0)
+    mine = buf[start:start + n]  # this rank's messages [start, start + n) of the global batch
+    fn = lambda: engine.highway_batch(key, msgs, 64, 4, out=mine)  # noqa: E731
+    plane.barrier()
+    ms = _event_ms(fn, max(3, args.steps // 2), 2, stream)
+    peer.fence()
+    t = plane.max(float(np.mean(ms)))
+    del mine, buf
+    peer.fence()
+    return {"what": "each rank's kernel stores its digests into rank 0's buffer (peer.py)",
+            "ms_per_step": round(t, 4)}
 
 
 def run_e2e(args, plane: Plane, key, dev, start: int, n_rank: int):
