@@ -497,7 +497,8 @@ def run_ours(args):
     gather = None
     if ws > 1:
         gather = gather_digests_timed(plane, out, dev)
-        gather["peer_stores"] = peer_store_steps(args, plane, key, msgs, start, n, stream)
+        if args.peer_gather:  # opt-in: maps rank 0's buffer into every rank (CUDA IPC)
+            gather["peer_stores"] = peer_store_steps(args, plane, key, msgs, start, n, stream)
     e2e = run_e2e(args, plane, key, dev, start, n)
     result = None
     if rank == 0:
@@ -733,6 +734,8 @@ def parse(argv=None):
     ap.add_argument("--config-steps", type=int, default=20)
     ap.add_argument("--config-cpu-seconds", type=float, default=1.0)
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--peer-gather", action="store_true",
+                    help="N > 1: also time the step with digests stored into rank 0 (peer.py)")
     ap.add_argument("--no-sustained", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clock-sampler", action="store_true")
