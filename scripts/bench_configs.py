@@ -43,18 +43,29 @@ def peak_gbs():
         return 6650.0
 
 
-def _time(fn, steps, warmup):
+SETTLE_S = 1.0  # idle before each row, so none inherits an earlier one's power-cap clocks
+LAST_CLOCKS: dict = {}
+
+
+def _time(fn, steps, warmup, settle=0.0):
     torch.cuda.synchronize()
+    if settle:
+        time.sleep(settle)
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-    ev[0].record(st)
-    for i in range(steps):
-        fn()
-        ev[i + 1].record(st)
-    torch.cuda.synchronize()
+    from bench import ClockSampler
+
+    with ClockSampler(torch.cuda.current_device(), period=0.005) as clk:
+        ev[0].record(st)
+        for i in range(steps):
+            fn()
+            ev[i + 1].record(st)
+        torch.cuda.synchronize()
+    LAST_CLOCKS.clear()
+    LAST_CLOCKS.update(clk.summary())
     return float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]))
 
 
@@ -85,7 +96,8 @@ def _graph_time(fn, per_graph=16, reps=10):
 
 
 def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, calls, verbose):
-    ms = _time(fn, steps, warmup)
+    ms = _time(fn, steps, warmup, SETTLE_S)
+    clocks = dict(LAST_CLOCKS)
     call_ms = None
     if bound == "latency":
         # Small batches: a Python call costs more than its kernel; the
@@ -113,6 +125,7 @@ def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, ca
     r["roofline"]["frac"] = (r["roofline"]["hbm_frac"] if bound == "hbm" else
                              r["roofline"].get("int_pipe", {}).get("frac_balanced"))
     r["cpu_baseline"] = cpu
+    r["clocks"] = {k: clocks.get(k) for k in ("sm_mhz", "reasons", "samples")}
     if verbose:
         print(json.dumps(r), flush=True)
     return r
