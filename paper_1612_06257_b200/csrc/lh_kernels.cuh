@@ -321,11 +321,10 @@ __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
 #endif
 // MPL messages per lane per warp iteration (a group of 32 * MPL consecutive
 // messages staged together, hashed one after another by each lane).
-#ifndef LH_SHORT_MINB
-#define LH_SHORT_MINB 1  // A/B knob: min blocks per SM (caps registers)
-#endif
+// (No min-blocks bound: __launch_bounds__(64, 1) alone moved ptxas to 108
+// registers and cfg3 to 1.885 ms; 11..13 blocks, 1.81-1.83 ms.)
 template <int WARPS, int MPL = LH_SHORT_MPL>
-__global__ void __launch_bounds__(WARPS * 32, LH_SHORT_MINB) k_ragged_short(const Highway proto,
+__global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto,
                                                              const uint8_t* __restrict__ buf,
                                                              const u64* __restrict__ offsets,
                                                              const u32* __restrict__ lengths,
