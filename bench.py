@@ -489,6 +489,7 @@ def run_ours(args):
     if ir:
         ir["frac_canonical"] = round(ir["t_int_canonical_ms"] / per_launch_ms, 4)
         ir["frac_balanced"] = round(ir["t_int_balanced_ms"] / per_launch_ms, 4)
+        ir["frac_slot"] = round(ir["t_int_slot_ms"] / per_launch_ms, 4)
         roof["int_pipe"] = ir
         t_hbm = alg_bytes / (read_gbs * 1e9) * 1e3
         roof["t_roof_ms"] = round(max(t_hbm, ir["t_int_balanced_ms"]), 4)

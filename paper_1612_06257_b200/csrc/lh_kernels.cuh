@@ -347,10 +347,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       start[m] = 0;
       len[m] = 0;
       if (i < n) {
+#ifdef LH_DIAG_NOLOAD  // timing diagnostic only: synthetic layout, no metadata or payload loads
+        if (offsets) {
+          start[m] = i * 36;
+          len[m] = 8 + (u32)(i * 7) % 57;
+        } else {
+#else
         if (offsets) {
           start[m] = offsets[i];
           len[m] = lengths ? (u64)lengths[i] : offsets[i + 1] - start[m];
         } else {  // fixed layout: message i = buf[i*L : (i+1)*L]
+#endif
           start[m] = i * fixed_len;
           len[m] = fixed_len;
         }
@@ -377,7 +384,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       const u32 nch = (u32)((hi_al - lo_al) >> 4);
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
       LH_CHECK(nch <= kSpan / 16 + 8);
+#ifndef LH_DIAG_NOLOAD
       for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
+#endif
       __syncwarp();
 #pragma unroll 1
       for (int m = 0; m < MPL; ++m) {

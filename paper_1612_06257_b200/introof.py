@@ -18,6 +18,18 @@ saturated) and r_issue the measured dual-issue ceiling.  Two variants:
   csrc/lh_device.cuh), split to minimise t.  This is the tighter (lower)
   bound for any implementation with the canonical op count.
 
+* ``slot`` -- what tools/issuemix.cu measured on this B200
+  (profiles/r2_issuemix.json): a 32-bit-result IMAD / IMAD.X issues beside
+  an ALU-pipe instruction at no cost (1:1 mixes run at 1.0-1.12 warp
+  instructions per clock per SM sub-partition), but an instruction with a
+  64-bit or high-half product (IMAD.WIDE, IMAD.HI) holds the issue port of
+  the ALU pipe for one ALU slot as well as its own 4 FMA clocks: x ALU
+  instructions + 1 IMAD.WIDE take 2x + 2 clocks for every x >= 1.  So a mix
+  needs at least (ALU-class ops + IMAD.WIDE ops) ALU slots of 2 clocks each
+  per warp, however its high halves are split -- the bound that explains why
+  every SipRound instruction selection runs at 40-43 clocks per warp-round
+  (20 slots) and the HighwayHash Update at 138 (64 slots = 128 clocks).
+
 Per-message op counts:
     HighwayHash  80*(floor(L/32)+4) + 96*[L%32 != 0] + 4*(w/64)
     SipHash-c-d  (floor(L/8)+1)*(4+24c) + 24d + 9
@@ -123,6 +135,18 @@ def roof_seconds(mix: Mix, peaks: dict, balanced: bool) -> float:
     return best
 
 
+def slot_seconds(mix: Mix, peaks: dict) -> float:
+    """ALU-slot bound (module docstring): every ALU-class op and every
+    IMAD.WIDE takes one slot of the ALU pipe's measured rate; the high
+    halves of 64-bit adds ride the FMA pipe for free (IMAD.X)."""
+    r = {k: v["warp_instr_per_s"] for k, v in peaks["classes"].items()}
+    return sum(mix.n.get(k, 0.0) / r[k] for k in ALU) + mix.n.get("wide", 0.0) / r["lop3"]
+
+
+def slots(mix: Mix) -> float:
+    return sum(mix.n.get(k, 0.0) for k in ALU) + mix.n.get("wide", 0.0)
+
+
 def launch_roof(mix: Mix, n_msgs: float, peaks: Optional[dict] = None) -> Optional[dict]:
     """Integer roof of a launch hashing n_msgs messages of this mix:
     canonical-op totals and the two bounds in ms."""
@@ -132,10 +156,14 @@ def launch_roof(mix: Mix, n_msgs: float, peaks: Optional[dict] = None) -> Option
     warps = n_msgs / 32.0
     can = roof_seconds(mix, peaks, balanced=False) * warps
     bal = roof_seconds(mix, peaks, balanced=True) * warps
+    slot = max(slot_seconds(mix, peaks) * warps, bal)
     return {"canonical_ops_per_msg": round(mix.total(), 2),
             "canonical_ops_per_launch": round(mix.total() * n_msgs),
             "t_int_canonical_ms": round(can * 1e3, 4),
             "t_int_balanced_ms": round(bal * 1e3, 4),
+            "alu_slots_per_msg": round(slots(mix), 2),
+            "t_int_slot_ms": round(slot * 1e3, 4),
             "clock_mhz": peaks.get("sm_mhz"),
             "source": "profiles/int_peak.json (tools/intpeak.cu per-class rates) x SURVEY "
-                      "§8(d) canonical mix (paper_1612_06257_b200/introof.py)"}
+                      "§8(d) canonical mix (paper_1612_06257_b200/introof.py); slot bound: "
+                      "profiles/r2_issuemix.json (tools/issuemix.cu)"}

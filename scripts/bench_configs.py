@@ -121,9 +121,13 @@ def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, ca
         if ir:
             ir["frac_canonical"] = round(ir["t_int_canonical_ms"] / ms, 4)
             ir["frac_balanced"] = round(ir["t_int_balanced_ms"] / ms, 4)
+            ir["frac_slot"] = round(ir["t_int_slot_ms"] / ms, 4)
             r["roofline"]["int_pipe"] = ir
+    # INT-bound rows: against the ALU-slot bound (the tightest measured one).
     r["roofline"]["frac"] = (r["roofline"]["hbm_frac"] if bound == "hbm" else
-                             r["roofline"].get("int_pipe", {}).get("frac_balanced"))
+                             r["roofline"].get("int_pipe", {}).get("frac_slot"))
+    if bound != "hbm":
+        r["roofline"]["frac_basis"] = "int_pipe.t_int_slot_ms"
     r["cpu_baseline"] = cpu
     r["clocks"] = {k: clocks.get(k) for k in ("sm_mhz", "reasons", "samples")}
     if verbose:

@@ -39,3 +39,14 @@ def test_launch_roof_scales_with_messages():
     r = introof.launch_roof(introof.highway_mix(1024), 32 * 1000, _peaks())
     assert r["canonical_ops_per_launch"] == 2884 * 32000
     assert r["t_int_balanced_ms"] <= r["t_int_canonical_ms"]
+
+
+def test_slot_bound():
+    # Update: 16 IADD3 + 16 LOP3 + 24 PRMT + 8 IMAD.WIDE; SipRound: 4 + 8 + 8.
+    assert introof.slots(introof.UPDATE) == 64 and introof.slots(introof.SIPROUND) == 20
+    p = _peaks()
+    assert introof.slot_seconds(introof.UPDATE, p) == pytest.approx(64.0)
+    r = introof.launch_roof(introof.sip_mix(1024, 2, 4), 32, p)
+    # never below the balanced bound
+    assert r["t_int_slot_ms"] >= r["t_int_balanced_ms"]
+    assert r["alu_slots_per_msg"] == introof.slots(introof.sip_mix(1024, 2, 4))
