@@ -319,6 +319,24 @@ __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
 #ifndef LH_SHORT_MPL
 #define LH_SHORT_MPL 4
 #endif
+// Staging copy of a warp's window: coalesced 16-byte chunks, global -> shared.
+// Asynchronous copies (LDGSTS.128: no registers, every chunk in flight at
+// once, one wait); the plain LDG -> STS loop runs in batches of 8 loads, each
+// batch a round trip (cfg3 1.778 -> 1.747 ms; LH_SHORT_NO_LDGSTS is the A/B knob).
+#ifndef LH_SHORT_NO_LDGSTS
+#define LH_STAGE_COPY(dst, src, nch, lane)                                                     \
+  do {                                                                                         \
+    const u32 d0_ = smem_u32(dst);                                                             \
+    for (u32 c = lane; c < nch; c += 32)                                                       \
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d0_ + 16 * c),            \
+                   "l"((src) + c)                                                              \
+                   : "memory");                                                                \
+    asm volatile("cp.async.wait_all;" ::: "memory");                                           \
+  } while (0)
+#else
+#define LH_STAGE_COPY(dst, src, nch, lane) \
+  for (u32 c = lane; c < nch; c += 32) (dst)[c] = __ldg((src) + c)
+#endif
 // MPL messages per lane per warp iteration (a group of 32 * MPL consecutive
 // messages staged together, hashed one after another by each lane).
 // (No min-blocks bound: __launch_bounds__(64, 1) alone moved ptxas to 108
@@ -385,7 +403,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
       LH_CHECK(nch <= kSpan / 16 + 8);
 #ifndef LH_DIAG_NOLOAD
-      for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
+      LH_STAGE_COPY(&stage[warp][0], src, nch, lane);
 #endif
       __syncwarp();
 #pragma unroll 1
@@ -588,7 +606,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_staged_any(const H proto,
       const u32 nch = (u32)((hi_al - lo_al) >> 4);
       const uint4* src = reinterpret_cast<const uint4*>(buf + lo_al);
       LH_CHECK(nch <= kSpan / 16 + 8);
-      for (u32 c = lane; c < nch; c += 32) stage[warp][c] = __ldg(src + c);
+      // cfg3-shaped SipHash-2-4 / -1-3: 2.000 -> 1.971 / 1.457 -> 1.391 ms vs LDG -> STS
+      LH_STAGE_COPY(&stage[warp][0], src, nch, lane);
       if constexpr (IsSipHash<H>::value) {
         __syncwarp();
         hash_sip_group<WARPS, MPL, SORT>(proto, S, start, len, base, n, lo_al, lane, warp, out);
