@@ -211,6 +211,46 @@ int lh_ragged_plan(const uint64_t* d_offsets, const uint32_t* d_lengths, uint64_
                    uint64_t chunk_msgs, uint64_t buf_len, uint64_t* d_lo,
                    uint64_t* d_hi, uint64_t* d_bad, void* stream);
 
+/* lh_ragged_plan plus the lane balance of the natural message order.  With
+ * work(i) = (len_i >> unit_shift) + fixed_units (32-byte packets + 5 for
+ * HighwayHash, 8-byte words + 3 for SipHash: the per-message finalization),
+ * d_stats[0] = sum of work and d_stats[1] = the sum over groups of 32
+ * consecutive messages of 32 * max work -- the lane-steps a one-message-per-
+ * lane kernel spends.  d_stats[0] / d_stats[1] is the warp efficiency of the
+ * natural order; the Python host calls lh_ragged_order when it is below 0.8.
+ * d_stats may be NULL (then identical to lh_ragged_plan). */
+int lh_ragged_plan_stats(const uint64_t* d_offsets, const uint32_t* d_lengths, uint64_t n,
+                         uint64_t chunk_msgs, uint64_t buf_len, uint64_t* d_lo, uint64_t* d_hi,
+                         uint64_t* d_bad, uint64_t* d_stats, unsigned unit_shift,
+                         unsigned fixed_units, void* stream);
+
+/* Length-class schedule of a ragged batch: d_sched[0..n) becomes the
+ * messages as 16-byte records {u64 offset, u32 length, u32 index} grouped by
+ * length class, longest first (classes of len >> unit_shift: exact below 128
+ * units, then 8 per octave), so that the 32 lanes of a warp of the ordered
+ * kernels hash messages of nearly equal length.  A length >= 2^32 - 1 is
+ * stored saturated (0xFFFFFFFF: the kernels re-read it from the layout).  A
+ * counting sort in three launches; d_sched = 16 * n bytes, 16-byte aligned;
+ * d_scratch = 1,024 u32 of device scratch.  n < 2^32.  The order inside a
+ * class is unspecified; digests do not depend on it.  Replaces: nothing in
+ * the reference (per-message calls have no lanes to balance). */
+int lh_ragged_order(const uint64_t* d_offsets, const uint32_t* d_lengths, uint64_t n,
+                    unsigned unit_shift, void* d_sched, uint32_t* d_scratch, void* stream);
+
+/* lh_highway_ragged / lh_siphash_ragged with a schedule: thread t hashes the
+ * message of record d_sched[t] (lh_ragged_order's output, or any permutation
+ * of the batch in that format) and writes its digest to d_out[index] -- the
+ * output is in message order, identical to the unordered calls.
+ * Register-ring kernel; n < 2^32. */
+int lh_highway_ragged_ordered(const uint8_t* d_buf, const uint64_t* d_offsets,
+                              const uint32_t* d_lengths, uint64_t n, const void* d_sched,
+                              const uint64_t key[4], int width, int rounds, uint64_t* d_out,
+                              void* stream);
+int lh_siphash_ragged_ordered(const uint8_t* d_buf, const uint64_t* d_offsets,
+                              const uint32_t* d_lengths, uint64_t n, const void* d_sched,
+                              const uint64_t key[2], int c, int d, int tree, uint64_t* d_out,
+                              void* stream);
+
 /* Seeded synthetic input generator (bench/test harness; not a reference
  * interface).  Byte b of the stream is byte (b & 7) of
  * word(seed, stream_id, word_offset + b / 8), see DESIGN.md §Synthetic

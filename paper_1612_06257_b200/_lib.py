@@ -70,6 +70,10 @@ def _declare(l):
     l.lh_sip_round_states.argtypes = [vp, u64, i32, vp]
     l.lh_ragged_plan.argtypes = [vp, vp, u64, u64, u64, vp, vp, vp, vp]
     l.lh_read_probe.argtypes = [vp, u64, vp, vp]
+    l.lh_ragged_plan_stats.argtypes = [vp, vp, u64, u64, u64, vp, vp, vp, vp, u32, u32, vp]
+    l.lh_ragged_order.argtypes = [vp, vp, u64, u32, vp, vp, vp]
+    l.lh_highway_ragged_ordered.argtypes = [vp, vp, vp, u64, vp, vp, i32, i32, vp, vp]
+    l.lh_siphash_ragged_ordered.argtypes = [vp, vp, vp, u64, vp, vp, i32, i32, i32, vp, vp]
     for name in (
         "lh_highway_fixed", "lh_highway_fixed_kernel", "lh_highway_ragged",
         "lh_highway_ragged_kernel", "lh_siphash_fixed", "lh_siphash_fixed_kernel",
@@ -78,7 +82,8 @@ def _declare(l):
         "lh_stream_init", "lh_stream_update", "lh_stream_finish", "lh_avalanche_counts",
         "lh_highway_update_states", "lh_highway_bijectivity",
         "lh_highway_remainder_states", "lh_highway_finalize_states", "lh_sip_round_states",
-        "lh_ragged_plan", "lh_read_probe",
+        "lh_ragged_plan", "lh_read_probe", "lh_ragged_plan_stats", "lh_ragged_order",
+        "lh_highway_ragged_ordered", "lh_siphash_ragged_ordered",
     ):
         getattr(l, name).restype = i32
 

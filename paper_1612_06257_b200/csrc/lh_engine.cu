@@ -222,6 +222,25 @@ int lh_siphash_fixed(const uint8_t* d_msgs, uint64_t n, uint64_t len, const uint
                                  LH_KERNEL_AUTO);
 }
 
+static int sip_ragged_impl(const uint8_t* d_buf, const uint64_t* d_offsets,
+                           const uint32_t* d_lengths, uint64_t n, const uint64_t key[2], int c,
+                           int d, int tree, uint64_t* d_out, cudaStream_t st, bool staged,
+                           const uint4* order) {
+  const bool r24 = c == 2 && d == 4, r13 = c == 1 && d == 3;
+  if (tree) {
+    if (r24)
+      return sip_ragged_t24(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged, order);
+    if (r13)
+      return sip_ragged_t13(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged, order);
+    return sip_ragged_t00(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged, order);
+  }
+  if (r24)
+    return sip_ragged_s24(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged, order);
+  if (r13)
+    return sip_ragged_s13(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged, order);
+  return sip_ragged_s00(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged, order);
+}
+
 int lh_siphash_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
                              const uint32_t* d_lengths, uint64_t n, const uint64_t key[2], int c,
                              int d, int tree, uint64_t* d_out, void* stream, int kernel) {
@@ -231,17 +250,37 @@ int lh_siphash_ragged_kernel(const uint8_t* d_buf, const uint64_t* d_offsets,
   if (kernel != LH_KERNEL_AUTO && kernel != LH_KERNEL_DIRECT && kernel != LH_KERNEL_RING &&
       kernel != LH_KERNEL_STAGED)
     return LH_EINVAL;
-  cudaStream_t st = (cudaStream_t)stream;
-  const bool staged = kernel == LH_KERNEL_STAGED;
-  const bool r24 = c == 2 && d == 4, r13 = c == 1 && d == 3;
-  if (tree) {
-    if (r24) return sip_ragged_t24(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged);
-    if (r13) return sip_ragged_t13(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged);
-    return sip_ragged_t00(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged);
-  }
-  if (r24) return sip_ragged_s24(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged);
-  if (r13) return sip_ragged_s13(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged);
-  return sip_ragged_s00(key, c, d, d_buf, d_offsets, d_lengths, n, d_out, st, staged);
+  return sip_ragged_impl(d_buf, d_offsets, d_lengths, n, key, c, d, tree, d_out,
+                         (cudaStream_t)stream, kernel == LH_KERNEL_STAGED, nullptr);
+}
+
+int lh_siphash_ragged_ordered(const uint8_t* d_buf, const uint64_t* d_offsets,
+                              const uint32_t* d_lengths, uint64_t n, const void* d_sched,
+                              const uint64_t key[2], int c, int d, int tree, uint64_t* d_out,
+                              void* stream) {
+  if (!key || c < 1 || d < 1 || (n && (!d_out || !d_offsets || !d_buf || !d_sched)))
+    return LH_EINVAL;
+  if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4 ||
+      (uintptr_t)d_sched % 16)
+    return LH_EALIGN;
+  if (n > 0xFFFFFFFFull) return LH_ETOOBIG;
+  return sip_ragged_impl(d_buf, d_offsets, d_lengths, n, key, c, d, tree, d_out,
+                         (cudaStream_t)stream, false, (const uint4*)d_sched);
+}
+
+int lh_highway_ragged_ordered(const uint8_t* d_buf, const uint64_t* d_offsets,
+                              const uint32_t* d_lengths, uint64_t n, const void* d_sched,
+                              const uint64_t key[4], int width, int rounds, uint64_t* d_out,
+                              void* stream) {
+  if (!key || !valid_width(width) || rounds < 0 ||
+      (n && (!d_out || !d_offsets || !d_buf || !d_sched)))
+    return LH_EINVAL;
+  if ((uintptr_t)d_out % 8 || (uintptr_t)d_offsets % 8 || (uintptr_t)d_lengths % 4 ||
+      (uintptr_t)d_sched % 16)
+    return LH_EALIGN;
+  if (n > 0xFFFFFFFFull) return LH_ETOOBIG;
+  const Highway h = make_highway(key, width, rounds);
+  return launch_ring(h, d_buf, d_offsets, d_lengths, 0, n, d_out, (cudaStream_t)stream, (const uint4*)d_sched);
 }
 
 int lh_siphash_ragged(const uint8_t* d_buf, const uint64_t* d_offsets, const uint32_t* d_lengths,

@@ -243,15 +243,26 @@ __global__ void __launch_bounds__(128) k_ragged_ring(const H proto, const uint8_
                                                      const u64* __restrict__ offsets,
                                                      const u32* __restrict__ lengths,
                                                      u64 fixed_len, u64 n,
-                                                     u64* __restrict__ out) {
+                                                     u64* __restrict__ out,
+                                                     const uint4* __restrict__ sched) {
   const int W = nout(proto);
   __shared__ __align__(16) ProtoSmem sp;
   const u32 sa = stage_proto(proto, sp);
   __syncthreads();
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (u64)gridDim.x * blockDim.x) {
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (u64)gridDim.x * blockDim.x) {
+    u64 i = t;
     u64 off, len;
-    if (offsets) {
+    if (sched) {
+      // Schedule record t (lh_ragged_order): {offset, length, message index},
+      // grouped by length class, so the lanes of a warp hold messages of
+      // nearly equal length.  A saturated length is re-read from the layout.
+      const uint4 r = __ldg(sched + t);
+      i = r.w;
+      off = pack(r.x, r.y);
+      len = r.z;
+      if (r.z == 0xFFFFFFFFu) len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
+    } else if (offsets) {
       off = offsets[i];
       len = lengths ? (u64)lengths[i] : offsets[i + 1] - off;
     } else {  // fixed layout: message i = buf[i*L : (i+1)*L]
@@ -1129,7 +1140,7 @@ static_assert(kRingDepth >= 2 && LH_FALLBACK_DEPTH >= 2,
 
 template <class H>
 int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u32* lengths,
-                u64 fixed_len, u64 n, u64* out, cudaStream_t st) {
+                u64 fixed_len, u64 n, u64* out, cudaStream_t st, const uint4* order = nullptr) {
   int sms = 0;
   int rc = check_device(&sms);
   if (rc) return rc;
@@ -1142,10 +1153,10 @@ int launch_ring(const H& proto, const uint8_t* buf, const u64* offsets, const u3
   const unsigned grid = grid_for(n, 128, sms);
   if constexpr (std::is_same<H, Highway>::value)
     k_ragged_ring<H, kRingDepth, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths,
-                                                             fixed_len, n, out);
+                                                             fixed_len, n, out, order);
   else
     k_ragged_ring<H, 4, 16><<<grid, 128, 0, st>>>(proto, buf, offsets, lengths, fixed_len, n,
-                                                    out);
+                                                    out, order);
   return cuda_err(cudaGetLastError());
 }
 
@@ -1452,7 +1463,9 @@ bool valid_width(int w) { return w == 64 || w == 128 || w == 256; }
 
 template <class H>
 int sip_dispatch_ragged(const H& h, const uint8_t* buf, const u64* off, const u32* lens, u64 n,
-                        u64* out, cudaStream_t st, bool staged = false) {
+                        u64* out, cudaStream_t st, bool staged = false,
+                        const uint4* order = nullptr) {
+  if (order) return launch_ring(h, buf, off, lens, 0, n, out, st, order);
   if (staged) return launch_staged_any(h, buf, off, lens, 0, n, out, st);
   // The register-ring reader is the Sip ragged kernel at every length: its
   // alignment-branch-free word reads beat the prefetching direct reader even

@@ -33,8 +33,8 @@ int LH_CAT(sip_fixed_, LH_VAR_TAG)(const u64 key[2], int c, int d, const uint8_t
 
 int LH_CAT(sip_ragged_, LH_VAR_TAG)(const u64 key[2], int c, int d, const uint8_t* buf,
                                     const u64* off, const u32* lens, u64 n, u64* out,
-                                    cudaStream_t st, bool staged) {
-  return sip_dispatch_ragged(make_var(key, c, d), buf, off, lens, n, out, st, staged);
+                                    cudaStream_t st, bool staged, const uint4* order) {
+  return sip_dispatch_ragged(make_var(key, c, d), buf, off, lens, n, out, st, staged, order);
 }
 
 // Streaming records carry runtime round counts: only the (0, 0) variants

@@ -22,7 +22,7 @@ namespace lh {
                       uint64_t len, uint64_t* out, cudaStream_t st, int kernel);              \
   int sip_ragged_##tag(const uint64_t key[2], int c, int d, const uint8_t* buf,               \
                        const uint64_t* off, const uint32_t* lens, uint64_t n, uint64_t* out,  \
-                       cudaStream_t st, bool staged);                                         \
+                       cudaStream_t st, bool staged, const uint4* order);                     \
   int sip_stream_tma_##tag(void* rec, const uint8_t* chunks, uint64_t n, uint64_t len,        \
                            cudaStream_t st);
 LH_SIP_VARIANTS(LH_SIP_DECLARE)

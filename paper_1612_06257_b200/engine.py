@@ -357,9 +357,18 @@ def _ragged_kernel(kind, kernel, span_bytes, n):
 
 
 def _launch_ragged(kind, key, buf_ptr, off_ptr, len_ptr, n, p1, p2, tree, out, device,
-                   kernel=KERNEL_AUTO):
+                   kernel=KERNEL_AUTO, order=None):
     st = _stream_ptr(device)
-    if kind == "hh":
+    if order is not None:  # length-class schedule (register-ring kernel)
+        if kind == "hh":
+            rc = _lib.lib().lh_highway_ragged_ordered(buf_ptr, off_ptr, len_ptr, n,
+                                                      order.data_ptr(), _key4(key), p1, p2,
+                                                      out.data_ptr(), st)
+        else:
+            rc = _lib.lib().lh_siphash_ragged_ordered(buf_ptr, off_ptr, len_ptr, n,
+                                                      order.data_ptr(), _key2(key), p1, p2, tree,
+                                                      out.data_ptr(), st)
+    elif kind == "hh":
         rc = _lib.lib().lh_highway_ragged_kernel(buf_ptr, off_ptr, len_ptr, n, _key4(key), p1,
                                                  p2, out.data_ptr(), st, kernel)
     else:
@@ -368,22 +377,90 @@ def _launch_ragged(kind, key, buf_ptr, off_ptr, len_ptr, n, p1, p2, tree, out, d
     _lib.check(rc, "ragged batch")
 
 
-def _plan(d_off, d_len, n: int, chunk_msgs: int, buf_len: int, device):
+# Work units of one message for the lane-balance statistic (lh_ragged_plan_stats):
+# (unit_shift, fixed_units) = 32-byte packets + 5 Updates of finalization and
+# remainder for HighwayHash; 8-byte words + 3 compressions for the Sip family.
+_WORK_UNITS = {"hh": (5, 5), "sip": (3, 3)}
+# Cost model of the automatic schedule (scripts/ragged_balance_bench.py, B200):
+# the ring kernels retire about 164 G HighwayHash lane-packets/s and 324 G
+# SipHash-2-4 lane-words/s; ordering costs ~15 us + 12 ps per message; an
+# ordered batch runs at ~0.93 warp efficiency.
+BALANCE_ORDERED_EFFICIENCY = 0.93
+BALANCE_COST_S = (15e-6, 12e-12)
+BALANCE_MARGIN = 1.2
+
+
+def _unit_seconds(kind, p1):
+    """Seconds per lane-step of the ring kernels (kind "sip": p1 = c rounds)."""
+    return 1 / 164e9 if kind == "hh" else (1.45e-12 * max(int(p1), 1) + 0.2e-12)
+
+
+def balance_gain(kind, p1, n, wsum, wmax32):
+    """(estimated seconds saved by the length-class schedule, its cost)."""
+    if not wmax32:
+        return 0.0, BALANCE_COST_S[0]
+    eff = wsum / wmax32
+    saved = wmax32 * _unit_seconds(kind, p1) * max(0.0, 1 - eff / BALANCE_ORDERED_EFFICIENCY)
+    return saved, BALANCE_COST_S[0] + BALANCE_COST_S[1] * n
+
+
+def _plan(d_off, d_len, n: int, chunk_msgs: int, buf_len: int, device, stats_kind=None):
     """lh_ragged_plan: per-chunk byte spans [lo, hi) and the invalid-message
     count of a device-resident layout, in one launch and one small D2H
-    (csrc/lh_plan.cu).  Raises ValueError for an invalid layout."""
+    (csrc/lh_plan.cu).  Raises ValueError for an invalid layout.  With
+    ``stats_kind`` ("hh" or "sip") also returns (sum of work, sum over
+    32-message groups of 32 * max work) of the natural order; their ratio is
+    its warp efficiency."""
     nchunks = -(-n // chunk_msgs)
-    res = torch.empty(2 * nchunks + 1, dtype=torch.int64, device=device)
-    rc = _lib.lib().lh_ragged_plan(d_off.data_ptr(), None if d_len is None else d_len.data_ptr(),
-                                   n, chunk_msgs, buf_len & 0xFFFFFFFFFFFFFFFF,
-                                   res.data_ptr(), res[nchunks:].data_ptr(),
-                                   res[2 * nchunks:].data_ptr(), _stream_ptr(device))
+    res = torch.empty(2 * nchunks + 3, dtype=torch.int64, device=device)
+    shift, fixed = _WORK_UNITS.get(stats_kind, (0, 0))
+    rc = _lib.lib().lh_ragged_plan_stats(
+        d_off.data_ptr(), None if d_len is None else d_len.data_ptr(), n, chunk_msgs,
+        buf_len & 0xFFFFFFFFFFFFFFFF, res.data_ptr(), res[nchunks:].data_ptr(),
+        res[2 * nchunks:].data_ptr(), res[2 * nchunks + 1:].data_ptr() if stats_kind else None,
+        shift, fixed, _stream_ptr(device))
     _lib.check(rc, "lh_ragged_plan")
     r = res.cpu().numpy().view(np.uint64)
-    if r[-1]:
-        raise ValueError(f"invalid ragged layout: {int(r[-1])} of {n} messages have decreasing "
-                         f"offsets, a wrapping length or end past the {buf_len}-byte buffer")
+    if r[2 * nchunks]:
+        raise ValueError(f"invalid ragged layout: {int(r[2 * nchunks])} of {n} messages have "
+                         f"decreasing offsets, a wrapping length or end past the {buf_len}-byte "
+                         "buffer")
+    if stats_kind:
+        return r[:nchunks], r[nchunks:2 * nchunks], (int(r[2 * nchunks + 1]), int(r[2 * nchunks + 2]))
     return r[:nchunks], r[nchunks:2 * nchunks]
+
+
+def ragged_order(d_off, d_len, n: int, kind: str = "hh"):
+    """lh_ragged_order: the batch as (n, 4) int32 schedule records {offset lo,
+    offset hi, length, message index} grouped by length class, longest first,
+    for the ordered ragged launches."""
+    device = d_off.device
+    sched = torch.empty((n, 4), dtype=torch.int32, device=device)
+    scratch = torch.empty(1024, dtype=torch.int32, device=device)
+    rc = _lib.lib().lh_ragged_order(d_off.data_ptr(), None if d_len is None else d_len.data_ptr(),
+                                    n, _WORK_UNITS["hh" if kind == "hh" else "sip"][0],
+                                    sched.data_ptr(), scratch.data_ptr(), _stream_ptr(device))
+    _lib.check(rc, "lh_ragged_order")
+    return sched
+
+
+def _schedule(kind, p1, d_off, d_len, n, buf_len, device, kern, check, balance):
+    """Layout validation and the lane-balance decision of one device-resident
+    ragged launch.  Returns the schedule tensor or None.  balance=None: order
+    the batch when the validation pass (check=True) measures a natural order
+    whose estimated loss exceeds BALANCE_MARGIN x the cost of ordering
+    (balance_gain); True: always (ring-kernel launches); False: never."""
+    ring = kern in (KERNEL_RING, KERNEL_DIRECT) and n < (1 << 32)
+    capturing = torch.cuda.is_current_stream_capturing()
+    sk = "hh" if kind == "hh" else "sip"
+    auto = balance is None and ring
+    want = balance is True and ring
+    if check and not capturing:
+        r = _plan(d_off, d_len, n, n, buf_len, device, sk if auto else None)
+        if auto:
+            saved, cost = balance_gain(sk, p1, n, *r[2])
+            want = saved > BALANCE_MARGIN * cost
+    return ragged_order(d_off, d_len, n, sk) if want else None
 
 
 def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, device,
@@ -446,7 +523,8 @@ def _ragged_host_pipelined(kind, key, buf, offsets, lengths, p1, p2, tree, lanes
     return to_u64(out_host)
 
 
-def _ragged_fast(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out, kernel, check):
+def _ragged_fast(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out, kernel, check,
+                 balance=None):
     """The common launch-bound call -- contiguous CUDA tensors of the right
     dtypes on the current device -- in one ctypes call (the general path's
     conversions cost more than a small kernel).  None if not applicable."""
@@ -474,18 +552,19 @@ def _ragged_fast(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out, ker
           or out.shape != _out_shape(n, lanes) or not out.is_contiguous()):
         _check_out(out, n, lanes, device)
     if n:
-        if check and not torch.cuda.is_current_stream_capturing():
-            _plan(offsets, lengths, n, n, buf.numel(), device)
+        kern = _ragged_kernel(kind, kernel, buf.numel(), n)
+        order = _schedule(kind, p1, offsets, lengths, n, buf.numel(), device, kern, check, balance)
         bp = buf.data_ptr() if buf.numel() else offsets.data_ptr()
         _launch_ragged(kind, key, bp, offsets.data_ptr(),
                        None if lengths is None else lengths.data_ptr(), n, p1, p2, tree, out,
-                       device, _ragged_kernel(kind, kernel, buf.numel(), n))
+                       device, kern, order)
     return out
 
 
 def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
-            kernel=KERNEL_AUTO, check=True):
-    r = _ragged_fast(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out, kernel, check)
+            kernel=KERNEL_AUTO, check=True, balance=None):
+    r = _ragged_fast(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out, kernel, check,
+                     balance)
     if r is not None:
         return r
     device = _require_cuda()
@@ -518,12 +597,13 @@ def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
     if n:
         # Host inputs are always checked (one extra sync is noise there).  A
         # layout being captured into a CUDA graph cannot be read back: trusted.
-        if (check or host) and not torch.cuda.is_current_stream_capturing():
-            _plan(d_off, d_len, n, n, d_buf.numel(), device)
+        kern = _ragged_kernel(kind, kernel, d_buf.numel(), n)
+        order = _schedule(kind, p1, d_off, d_len, n, d_buf.numel(), device, kern, check or host,
+                          balance)
         bp = d_buf.data_ptr() if d_buf.numel() else d_off.data_ptr()
         lp = d_len.data_ptr() if d_len is not None else None
-        _launch_ragged(kind, key, bp, d_off.data_ptr(), lp, n, p1, p2, tree, out, device,
-                       _ragged_kernel(kind, kernel, d_buf.numel(), n))
+        _launch_ragged(kind, key, bp, d_off.data_ptr(), lp, n, p1, p2, tree, out, device, kern,
+                       order)
     if host:
         return to_u64(out)
     return out
@@ -531,7 +611,7 @@ def _ragged(kind, key, buf, offsets, lengths, p1, p2, tree, lanes, out=None,
 
 def highway_ragged(key, buf, offsets, lengths=None, width: int = 64, rounds: int = 4,
                    out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO,
-                   check: bool = True):
+                   check: bool = True, balance: Optional[bool] = None):
     """HighwayHash over a packed ragged buffer.  Message i is
     buf[offsets[i] : offsets[i] + len_i] with len_i = lengths[i] when given,
     else offsets[i+1] - offsets[i] (offsets then holds n+1 entries).
@@ -543,23 +623,30 @@ def highway_ragged(key, buf, offsets, lengths=None, width: int = 64, rounds: int
     costs one metadata pass and a sync; check=False skips it for CUDA inputs
     the caller has validated (the C ABI's contract: offsets are trusted).
     Host inputs are always checked; calls captured into a CUDA graph are not
-    (nothing can be read back during capture)."""
+    (nothing can be read back during capture).
+    balance: the lane schedule of register-ring launches.  One message per
+    lane means a warp runs until its longest message is done; None (default)
+    lets the validation pass measure the natural order's warp efficiency and,
+    when the estimated loss outweighs the cost of ordering (balance_gain),
+    hashes the messages grouped by length class (lh_ragged_order; digests
+    stay in message order).  True always orders,
+    False never; with check=False nothing is measured, so None means False."""
     _check_width(width)
     if rounds < 0:
         raise ValueError("rounds must be >= 0")
     return _ragged("hh", as_key256(key), buf, offsets, lengths, width, rounds, 0,
-                   width // 64, out, kernel, check)
+                   width // 64, out, kernel, check, balance)
 
 
 def sip_ragged(key, buf, offsets, lengths=None, c: int = 2, d: int = 4, tree: bool = False,
                out: Optional[torch.Tensor] = None, kernel: int = KERNEL_AUTO,
-               check: bool = True):
-    """SipHash-c-d / SipTreeHash over a packed ragged buffer (layout and
-    ``check`` as highway_ragged)."""
+               check: bool = True, balance: Optional[bool] = None):
+    """SipHash-c-d / SipTreeHash over a packed ragged buffer (layout,
+    ``check`` and ``balance`` as highway_ragged)."""
     if c < 1 or d < 1:
         raise ValueError("round counts must be positive")
     return _ragged("sip", as_key128(key), buf, offsets, lengths, c, d, int(bool(tree)), 1, out,
-                   kernel, check)
+                   kernel, check, balance)
 
 
 # ---------------------------------------------------------------------------
