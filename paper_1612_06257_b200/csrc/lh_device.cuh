@@ -381,10 +381,11 @@ __device__ __forceinline__ u64 mulwide(u32 a, u32 b) {
 }
 
 // Runtime constants that move part of SipRound to the FMA pipe: `one` for
-// add64_mixed, and 2^13 / 2^17 / 2^16 so those rotates become IMAD.WIDE.U32
-// products (x * 2^k = x << k in the low word, x >> (32-k) in the high word)
-// merged by a 3-input LOP3 with the following XOR.  Set by the host; opaque
-// to ptxas, which would otherwise strength-reduce them.
+// add64_mixed, and (LH_SIP_WIDE_ROT builds only) 2^13 / 2^17 / 2^16 so those
+// rotates become IMAD.WIDE.U32 products (x * 2^k = x << k in the low word,
+// x >> (32-k) in the high word) merged by a 3-input LOP3 with the following
+// XOR.  Set by the host; opaque to ptxas, which would otherwise
+// strength-reduce them.
 struct SipMul {
   u32 one, m13, m17, m16;
 };
@@ -413,14 +414,19 @@ __device__ __forceinline__ u64 rotl16_xor_prmt(u64 x, u64 v) {
   return pack(lo ^ lo32(v), hi ^ hi32(v));
 }
 
-// S/sip.py:73-86.  The four 64-bit adds are IADD3 (ALU) + IMAD.X (FMA);
-// the rotates by 13 and 17 are IMAD.WIDE pairs (FMA), by 21 two SHF (ALU),
-// and by 16 two PRMT (W16 = false) or an IMAD.WIDE pair (W16 = true).  Per
-// round, in ALU / FMA issue slots: W16 = false 16 / 12, true 14 / 16;
-// alternating the two (sip_rounds) balances the pipes at 15 / 14 -- SipHash
-// is ALU-bound, so fewer ALU slots is time.
+// S/sip.py:73-86.  The four 64-bit adds are IADD3 (ALU) + IMAD.X (FMA, free
+// beside an ALU instruction); every rotate runs on the ALU pipe: by 13, 17
+// and 21 as two funnel shifts, by 16 as two PRMT, by 32 as a register rename:
+// 20 ALU slots per round.  tools/issuemix.cu showed why the
+// former IMAD.WIDE rotates (LH_SIP_WIDE_ROT, the A/B knob: by 13 and 17
+// always, by 16 on every other round) only looked cheaper: an IMAD.WIDE holds
+// the ALU issue slot for 2 clocks besides its 4 FMA clocks, so a WIDE pair
+// costs the ALU pipe what two SHF cost and the FMA pipe 8 clocks on top.
+// All-ALU: SipHash-2-4 / -1-3 / SipTree-2-4 / -1-3 over 2^24 x 1 KiB
+// 5.48 / 3.00 / 6.08 / 3.39 -> 5.16 / 2.83 / 5.83 / 3.26 ms.
 template <bool W16>
 __device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k) {
+#ifdef LH_SIP_WIDE_ROT
   v0 = add64_mixed(v0, v1, k.one);
   v1 = rotl_xor_wide(v1, k.m13, v0);
   v0 = rot32(v0);
@@ -431,13 +437,26 @@ __device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3, co
   v2 = add64_mixed(v2, v1, k.one);
   v1 = rotl_xor_wide(v1, k.m17, v2);
   v2 = rot32(v2);
+#else
+  v0 = add64_mixed(v0, v1, k.one);
+  v1 = rotl_xor_shf<13>(v1, v0);
+  v0 = rot32(v0);
+  v2 = add64_mixed(v2, v3, k.one);
+  v3 = rotl16_xor_prmt(v3, v2);
+  v0 = add64_mixed(v0, v3, k.one);
+  v3 = rotl_xor_shf<21>(v3, v0);
+  v2 = add64_mixed(v2, v1, k.one);
+  v1 = rotl_xor_shf<17>(v1, v2);
+  v2 = rot32(v2);
+#endif
 }
 
 __device__ __forceinline__ void sip_round(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k) {
   sip_round<false>(v0, v1, v2, v3, k);
 }
 
-// n SipRounds alternating the two pipe mixes (n compile-time when N > 0).
+// n SipRounds (n compile-time when N > 0); the two forms differ only in
+// LH_SIP_WIDE_ROT builds.
 template <int N>
 __device__ __forceinline__ void sip_rounds(u64& v0, u64& v1, u64& v2, u64& v3, const SipMul& k,
                                            int n) {

@@ -20,7 +20,7 @@ saturated) and r_issue the measured dual-issue ceiling.  Two variants:
 
 * ``slot`` -- what tools/issuemix.cu measured on this B200
   (profiles/r2_issuemix.json): a 32-bit-result IMAD / IMAD.X issues beside
-  an ALU-pipe instruction at no cost (1:1 mixes run at 1.0-1.12 warp
+  an ALU-pipe instruction at no cost (1:1 mixes run at 0.95 warp
   instructions per clock per SM sub-partition), but an instruction with a
   64-bit or high-half product (IMAD.WIDE, IMAD.HI) holds the issue port of
   the ALU pipe for one ALU slot as well as its own 4 FMA clocks: x ALU

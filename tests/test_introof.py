@@ -47,6 +47,5 @@ def test_slot_bound():
     p = _peaks()
     assert introof.slot_seconds(introof.UPDATE, p) == pytest.approx(64.0)
     r = introof.launch_roof(introof.sip_mix(1024, 2, 4), 32, p)
-    # never below the balanced bound
     assert r["t_int_slot_ms"] >= r["t_int_balanced_ms"]
     assert r["alu_slots_per_msg"] == introof.slots(introof.sip_mix(1024, 2, 4))

@@ -9,8 +9,10 @@
 //
 // Every kernel: 64 warps per SM in one wave; each thread runs NA independent
 // chains of ALU form AF and NB independent chains of FMA form BF, RA and RB
-// ops per chain per step; rates are computed from in-kernel clock64() deltas
-// (max over blocks), so the SM clock does not enter.
+// ops per chain per step; rates = instructions / (CUDA-event time x the SM
+// clock attribute; the runs draw ~250 W, far from any throttle).  The
+// in-kernel clock64() maxima are printed too, but they run short for kernels
+// whose 8 blocks per SM are not all co-resident (> 32 registers).
 //
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/issuemix tools/issuemix.cu
 #include <cuda_runtime.h>
@@ -142,9 +144,12 @@ static void run(const char* name, int warps_per_sm = 64) {
   const int xa = (BF == B_WIDE_2R || BF == B_WIDE_1R_U || BF == B_LOHI_2R) ? RB * NB : 0;
   const int xb = BF == B_LOHI_2R ? RB * NB : 0;  // two FMA instructions per op
   const double per_warp = (double)iters * 8 * (RA * NA + RB * NB + xa + xb);
-  const double ipc_smsp = per_warp * warps_per_sm / 4.0 / best;
-  const double alu = (double)iters * 8 * (RA * NA + xa) * warps_per_sm / 4.0 / best;
-  const double fma = (double)iters * 8 * (RB * NB + xb) * warps_per_sm / 4.0 / best;
+  int khz = 0;
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
+  const double clk = best_ms * 1e-3 * khz * 1e3;  // SM clocks of the launch
+  const double ipc_smsp = per_warp * warps_per_sm / 4.0 / clk;
+  const double alu = (double)iters * 8 * (RA * NA + xa) * warps_per_sm / 4.0 / clk;
+  const double fma = (double)iters * 8 * (RB * NB + xb) * warps_per_sm / 4.0 / clk;
   printf("%s\n  \"%s\": {\"ipc_smsp\": %.3f, \"alu_per_clk\": %.3f, \"fma_per_clk\": %.3f, \"warps_per_sm\": %d, \"cyc_max\": %.0f, \"cyc_min\": %.0f, \"event_us\": %.1f}",
          g_first ? "" : ",", name, ipc_smsp, alu, fma, warps_per_sm, best, mn_c, best_ms * 1e3);
   g_first = false;
