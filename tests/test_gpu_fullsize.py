@@ -261,5 +261,33 @@ def test_ragged_offsets_past_4gib(oracle):
     got = to_u64(engine.sip_ragged(synth.key128(), buf, d_off, d_len, 2, 4))
     assert np.array_equal(got, oracle.batch_ragged(oracle.ALG_SIPHASH, synth.key128(), span, rel,
                                                    lens, 2, 4))
+    # the same batch through the length-class schedule (u64 offsets in the records)
+    got = to_u64(engine.highway_ragged(synth.key256(), buf, d_off, d_len, 64, kernel=KERNEL_RING,
+                                       balance=True))
+    assert np.array_equal(got, want)
     del buf
+    torch.cuda.empty_cache()
+
+
+def test_ordered_message_of_4gib(oracle):
+    """A message of 2^32 + 37 bytes in an ordered launch: its schedule record
+    holds a saturated length (0xFFFFFFFF) and the kernel re-reads the real one
+    from the layout; two short neighbours check the record order.  (One GPU
+    thread walks the 4 GiB message: ~13 s; the Sip kernels share the code.)"""
+    from paper_1612_06257_b200.engine import KERNEL_RING
+    big = (1 << 32) + 37
+    total = 100 + big + 500
+    if torch.cuda.get_device_properties(0).total_memory < 2.5 * total:
+        pytest.skip("needs more device memory")
+    buf = _fill(total, 29)
+    off = np.array([0, 100, 100 + big, total], np.uint64)
+    host = buf.cpu().numpy()
+    want = oracle.batch_ragged(oracle.ALG_HIGHWAY, synth.key256(), host, off, None, 256, 4)
+    d_off = torch.from_numpy(off.view(np.int64)).to(DEV)
+    sched = engine.ragged_order(d_off, None, 3, "hh").cpu().numpy().view(np.uint32)
+    assert sched[0, 3] == 1 and sched[0, 2] == 0xFFFFFFFF  # the long message first, saturated
+    got = engine.highway_ragged(synth.key256(), buf, d_off, None, 256, kernel=KERNEL_RING,
+                                balance=True)
+    assert np.array_equal(to_u64(got).reshape(want.shape), want)
+    del buf, host
     torch.cuda.empty_cache()

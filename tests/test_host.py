@@ -216,3 +216,22 @@ def test_cli_size_range_parsing():
     parser = cli.build_parser()
     assert cli._parse_sizes(parser, "4..6") == [4, 5, 6]
     assert cli._parse_sizes(parser, "1,8..10,32") == [1, 8, 9, 10, 32]
+
+
+def test_balance_cost_model():
+    """engine.balance_gain: nothing to gain from a balanced batch, more from
+    an unbalanced one, and a small batch never pays for its ordering."""
+    from paper_1612_06257_b200 import engine
+
+    n = 1 << 20
+    saved, cost = engine.balance_gain("hh", 4, n, wsum=37 * n, wmax32=37 * n)
+    assert saved == 0.0 and cost > 0
+    # U[0, 2048]-like: efficiency 0.55
+    s1, c1 = engine.balance_gain("hh", 4, n, wsum=37 * n, wmax32=int(37 * n / 0.55))
+    assert s1 > engine.BALANCE_MARGIN * c1
+    s2, _ = engine.balance_gain("sip", 2, n, wsum=131 * n, wmax32=int(131 * n / 0.55))
+    assert s2 > s1  # SipHash-2-4 spends more per byte
+    # 1,000 messages: the fixed cost dominates
+    s3, c3 = engine.balance_gain("hh", 4, 1000, wsum=37 * 1000, wmax32=int(37 * 1000 / 0.5))
+    assert s3 < c3
+    assert engine.balance_gain("hh", 4, 0, 0, 0) == (0.0, engine.BALANCE_COST_S[0])
