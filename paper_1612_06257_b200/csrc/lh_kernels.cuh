@@ -495,8 +495,8 @@ struct IsSipHash<Sip<C, D>> {
 //  * one flat loop over a key's whole words, then its final word -- at
 //    most 9 compressions per round (8 whole words + the length word)
 //    instead of absorb32 blocks plus tail words (up to 12);
-//  * (SORT: ragged launches) the group's keys are first ranked by length class (len >> 4: 0-15, 16-31, 32-47,
-//    48-63, 64 bytes; invalid slots last) with warp ballots and re-dealt to
+//  * (SORT: ragged launches) the group's keys are first ranked by length class (8-byte classes, or 16-byte
+//    ones for SipHash-1-3; invalid slots last) with warp ballots and re-dealt to
 //    the rounds through shared memory, so each round's lanes hash keys of
 //    similar length.  cfg3-shaped SipHash-2-4 2.45 -> 2.19 ms (flat loop)
 //    -> 2.00 ms (sorted).  Fixed rows (one length) keep the flat loop: the
@@ -523,16 +523,21 @@ __device__ __forceinline__ void hash_sip_group(const Sip<C, D>& proto, const u32
     __shared__ u64 s_start[WARPS][G];
     __shared__ u32 s_len[WARPS][G];
     __shared__ uint16_t s_slot[WARPS][G];
+    // Length classes of one word for 2+ rounds per word, two words for
+    // SipHash-1-3 (cfg3-shaped 2-4: 1.861 -> 1.810 ms with one-word classes;
+    // 1-3: 1.335 -> 1.390, the extra ballots cost more than they save).
+    constexpr u32 kSortShift = C == 1 ? 4 : 3;
+    constexpr u32 kSortMax = 64u >> kSortShift;  // class of a 64-byte key
     u32 cls[MPL];
 #pragma unroll
     for (int m = 0; m < MPL; ++m) {
       const u32 L = (u32)len[m];
-      cls[m] = base + 32 * m + lane < n ? min(L >> 4, 4u) : 5u;
+      cls[m] = base + 32 * m + lane < n ? min(L >> kSortShift, kSortMax) : kSortMax + 1;
     }
     const u32 lt = (1u << lane) - 1u;
     u32 pos[MPL], next = 0;
 #pragma unroll
-    for (u32 c = 0; c < 6; ++c) {
+    for (u32 c = 0; c < kSortMax + 2; ++c) {
 #pragma unroll
       for (int m = 0; m < MPL; ++m) {
         const u32 b = __ballot_sync(0xffffffffu, cls[m] == c);
