@@ -1030,6 +1030,12 @@ __global__ void __launch_bounds__(32, MINB)
 // Host helpers
 // --------------------------------------------------------------------------
 
+// Status of the launch just issued.  The library links the CUDA runtime
+// statically, so the "last error" cudaGetLastError reads and clears is this
+// library's own (per host thread): it cannot consume a launch error that
+// belongs to the caller's runtime (PyTorch's, say).  A sticky context error
+// (an earlier kernel's illegal address) is not cleared by it and keeps
+// failing every CUDA call of every runtime in the process, this one's too.
 int cuda_err(cudaError_t e) { return e == cudaSuccess ? LH_OK : LH_ECUDA; }
 
 // The device checks run on every call; the SM count and the compute
