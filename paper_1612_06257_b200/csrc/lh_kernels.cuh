@@ -352,8 +352,15 @@ __device__ __forceinline__ void rem_tweak(Highway& h, u32 r) {
 // messages staged together, hashed one after another by each lane).
 // (No min-blocks bound: __launch_bounds__(64, 1) alone moved ptxas to 108
 // registers and cfg3 to 1.885 ms; 11..13 blocks, 1.81-1.83 ms.)
+#if defined(LH_SHORT_MINB)  // A/B: a minimum-blocks bound (register cap)
+#define LH_SHORT_BOUNDS __launch_bounds__(WARPS * 32, LH_SHORT_MINB)
+#elif defined(LH_SHORT_MAXNREG)  // A/B: an explicit register cap
+#define LH_SHORT_BOUNDS __maxnreg__(LH_SHORT_MAXNREG)
+#else
+#define LH_SHORT_BOUNDS __launch_bounds__(WARPS * 32)
+#endif
 template <int WARPS, int MPL = LH_SHORT_MPL>
-__global__ void __launch_bounds__(WARPS * 32) k_ragged_short(const Highway proto,
+__global__ void LH_SHORT_BOUNDS k_ragged_short(const Highway proto,
                                                              const uint8_t* __restrict__ buf,
                                                              const u64* __restrict__ offsets,
                                                              const u32* __restrict__ lengths,
