@@ -287,22 +287,32 @@ struct HighwayHalf {
     half = h;
   }
 
+  // LH_SPLIT_PLAIN_ADD (A/B): plain 64-bit adds in the split kernel, which is
+  // bound by the latency of the Update chain, not by ALU slots.
+  __device__ __forceinline__ u64 add_(u64 a, u64 b) const {
+#ifdef LH_SPLIT_PLAIN_ADD
+    return a + b;
+#else
+    return add64_mixed(a, b, one);
+#endif
+  }
+
   __device__ __forceinline__ void update(u64 pa, u64 pb) {
     const u64 p[2] = {pa, pb};
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       v1[i] += p[i] + m0[i];  // 3-input IADD3 + IADD3.X: 2 instructions, no FMA-pipe help needed
       m0[i] ^= mul_lo_hi(v1[i], v0[i]);
-      v0[i] = add64_mixed(v0[i], m1[i], one);
+      v0[i] = add_(v0[i], m1[i]);
       m1[i] ^= mul_lo_hi(v0[i], v1[i]);
     }
     u64 z0, z1;
     zipper(v1[0], v1[1], z0, z1);
-    v0[0] = add64_mixed(v0[0], z0, one);
-    v0[1] = add64_mixed(v0[1], z1, one);
+    v0[0] = add_(v0[0], z0);
+    v0[1] = add_(v0[1], z1);
     zipper(v0[0], v0[1], z0, z1);
-    v1[0] = add64_mixed(v1[0], z0, one);
-    v1[1] = add64_mixed(v1[1], z1, one);
+    v1[0] = add_(v1[0], z0);
+    v1[1] = add_(v1[1], z1);
   }
 
   // t: the full 32-byte tail (both threads hold it), r = len % 32.

@@ -289,6 +289,23 @@ int main() {
   const int ublocks = sms * 2, uiters = 8192;  // 16 warps per SM, as the bench kernel
   float ms = time_ms([&] { k_update<<<ublocks, 256>>>(proto, (u64*)d, uiters); });
   const double updates = (double)ublocks * 256 * uiters / (ms * 1e-3);
+  // The same Update at low occupancy (long-message shards leave 1-2 warps per
+  // sub-partition): clocks per warp-Update at 4, 8, 16 and 32 warps per SM.
+  {
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
+    printf(" \"update_clk_per_warp_by_warps_per_sm\": {");
+    const int shapes[4][2] = {{1, 128}, {1, 256}, {2, 256}, {4, 256}};
+    for (int k = 0; k < 4; ++k) {
+      const int nb = sms * shapes[k][0], th = shapes[k][1];
+      const float m = time_ms([&] { k_update<<<nb, th>>>(proto, (u64*)d, uiters); });
+      const int wps = shapes[k][0] * th / 32;  // warps per SM
+      // each sub-partition runs wps/4 warps; a warp-Update then takes:
+      const double clk = m * 1e-3 * khz * 1e3 / uiters;
+      printf("%s\"%d\": %.1f", k ? ", " : "", wps, clk);
+    }
+    printf("},\n");
+  }
   const SipMul km{1u, 1u << 13, 1u << 17, 1u << 16};
   const int sblocks = sms * 8, siters = 4096;
   ms = time_ms([&] { k_sipround<<<sblocks, 256>>>(km, (u64*)d, siters); });
