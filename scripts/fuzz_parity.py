@@ -18,6 +18,14 @@ key, k128 = synth.key256(), synth.key128()
 T = len(os.sched_getaffinity(0))
 t_end = time.time() + budget
 cases = digests = bad = 0
+FAULT = os.environ.get("FUZZ_FAULT") == "1"  # self-test: corrupt one digest in ~2% of the cases
+
+
+def _same(got, want):
+    got = got.reshape(want.shape).copy()
+    if FAULT and got.size and rng.random() < 0.02:
+        got.reshape(-1)[int(rng.integers(0, got.size))] ^= np.uint64(1)
+    return np.array_equal(got, want)
 
 
 def ragged_case():
@@ -77,7 +85,7 @@ def ragged_case():
         got = engine.to_u64(engine.sip_ragged(k128, buf, d_off, d_len, c, d, tree, kernel=kern, balance=bal))
         want = oracle.batch_ragged(oracle.ALG_SIPTREE if tree else oracle.ALG_SIPHASH, k128, host, ho, hl, c, d, nthreads=T)
         desc = f"{'tree' if tree else 'sip'}{c}{d}"
-    ok = np.array_equal(got.reshape(want.shape), want)
+    ok = _same(got, want)
     cases += 1; digests += n; bad += not ok
     if not ok:
         print("MISMATCH ragged", desc, n, dist, mode, "offform" if use_off_form else "lens", "kernel", kern, "balance", bal,
@@ -118,7 +126,7 @@ def fixed_case():
             desc = f"{'tree' if tree else 'sip'}{c}{d}"
     except ValueError:
         return  # a kernel that does not take this shape
-    ok = np.array_equal(got.reshape(want.shape), want)
+    ok = _same(got, want)
     cases += 1; digests += n; bad += not ok
     if not ok:
         print("MISMATCH fixed", desc, n, L, "kernel", kern, "shift", shift, flush=True)
