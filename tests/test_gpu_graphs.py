@@ -65,3 +65,26 @@ def test_ragged_and_sip_graph_replay(oracle):
                                                               None, 64, 4))
         assert np.array_equal(to_u64(o2), oracle.batch_ragged(oracle.ALG_SIPHASH, k2, host, off,
                                                               None, 2, 4))
+
+
+def test_ordered_ragged_graph_replay(oracle):
+    """balance=True inside a capture: the three ordering launches and the
+    ordered hashing launch replay together (the layout is fixed; the bytes
+    change between replays)."""
+    key = synth.key256()
+    lens = synth.lengths(6, 9000, 0, 3000)
+    off = np.zeros(9001, np.uint64)
+    off[1:] = np.cumsum(lens)
+    total = int(off[-1])
+    d_buf = torch.empty(total, dtype=torch.uint8, device="cuda")
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    out = torch.empty(9000, dtype=torch.int64, device="cuda")
+    g = _capture(lambda: engine.highway_ragged(key, d_buf, d_off, None, 64, out=out,
+                                               kernel=KERNEL_RING, balance=True))
+    for seed in (9, 10):
+        host = synth.counter_bytes(seed, total)
+        d_buf.copy_(torch.from_numpy(host))
+        g.replay()
+        torch.cuda.synchronize()
+        want = oracle.batch_ragged(oracle.ALG_HIGHWAY, key, host, off, None, 64, 4)
+        assert np.array_equal(to_u64(out), want), seed
