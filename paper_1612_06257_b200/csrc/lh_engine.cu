@@ -4,7 +4,7 @@
 #include "lh_kernels.cuh"
 #include "lh_sip_variants.h"
 
-#define LH_VERSION_STR "paper_1612_06257_b200 0.2.0 (sm_100a)"
+#define LH_VERSION_STR "paper_1612_06257_b200 0.3.0 (sm_100a)"
 
 namespace {
 
