@@ -95,7 +95,8 @@ def _graph_time(fn, per_graph=16, reps=10):
     return _time(g.replay, reps, 2) / per_graph
 
 
-def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, calls, verbose):
+def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, calls, verbose,
+         extra=None):
     ms = _time(fn, steps, warmup, SETTLE_S)
     clocks = dict(LAST_CLOCKS)
     call_ms = None
@@ -130,6 +131,7 @@ def _row(name, fn, steps, warmup, payload, nmsgs, alg_bytes, mix, cpu, bound, ca
         r["roofline"]["frac_basis"] = "int_pipe.t_int_slot_ms"
     r["cpu_baseline"] = cpu
     r["clocks"] = {k: clocks.get(k) for k in ("sm_mhz", "reasons", "samples")}
+    r.update(extra or {})
     if verbose:
         print(json.dumps(r), flush=True)
     return r
@@ -150,8 +152,8 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
     stay alive through the closures until the caller drops the list."""
     from oracle import oracle as orc
 
-    def _row_(*a):
-        return _row(*a, calls, verbose)
+    def _row_(*a, extra=None):
+        return _row(*a, calls, verbose, extra)
 
     key, k128 = synth.key256(), synth.key128()
     T = len(os.sched_getaffinity(0))
@@ -215,6 +217,40 @@ def run_all(dev, steps=20, warmup=3, cpu_seconds=1.0, only=None, calls=None, ver
                              steps, warmup, total, n, total + 20 * n,
                              _mean_mix(lambda L: introof.sip_mix(L, c, d), hl), cpu, "int"))
         if calls is None:  # else the closures keep the inputs for the profiler pass
+            del buf, lens, off, o
+            torch.cuda.empty_cache()
+
+    if on("ragged"):
+        # Not a BASELINE config: random-length ragged messages through the
+        # public call (validation + schedule decision + hashing), natural
+        # order vs the automatic length-class schedule.
+        n = 1 << 20
+        lens = torch.empty(n, dtype=torch.int32, device=dev)
+        synth.lengths_device(lens, 3, 0, 2048)
+        off = torch.zeros(n, dtype=torch.int64, device=dev)
+        off[1:] = torch.cumsum(lens[:-1].to(torch.int64), 0)
+        total = int(off[-1]) + int(lens[-1])
+        buf = torch.empty(total, dtype=torch.uint8, device=dev)
+        synth.fill_device(buf, 4)
+        o = torch.empty(n, dtype=torch.int64, device=dev)
+        hl = lens[: 1 << 18].cpu().numpy().view(np.uint32)
+        ho = off[: 1 << 18].cpu().numpy().view(np.uint64)
+        hb = orc.synth_fill(int(ho[-1]) + int(hl[-1]), 4, nthreads=T)
+        for name, kind, alg, c, d in (("hh64", "hh", orc.ALG_HIGHWAY, 64, 4),
+                                      ("siphash24", "sip", orc.ALG_SIPHASH, 2, 4)):
+            call = engine.highway_ragged if kind == "hh" else engine.sip_ragged
+            k = key if kind == "hh" else k128
+            cpu = _cpu(lambda: orc.batch_ragged(alg, k, hb, ho, hl, c, d, nthreads=T),
+                       len(hb), len(hl), "first 2^18 messages", cpu_seconds)
+            mix = _mean_mix((lambda L: introof.highway_mix(L, 64)) if kind == "hh" else
+                            (lambda L: introof.sip_mix(L, c, d)), hl)
+            nat = _time(partial(call, k, buf, off, lens, c, d, out=o, balance=False), steps,
+                        warmup)
+            r = _row_(f"ragged 2^20 x U[0,2048] {name} (checked call, automatic schedule)",
+                      partial(call, k, buf, off, lens, c, d, out=o), steps, warmup, total, n,
+                      total + 20 * n, mix, cpu, "int", extra={"ms_natural_order": round(nat, 4)})
+            rows.append(r)
+        if calls is None:
             del buf, lens, off, o
             torch.cuda.empty_cache()
 
