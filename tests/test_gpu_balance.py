@@ -123,3 +123,24 @@ def test_auto_schedule_orders_only_unbalanced_batches(monkeypatch):
     # a small batch: ordering would cost more than it saves
     engine.highway_ragged(key, d[0], d[1][:1000], d[2][:1000], 64)
     assert len(calls) == 1
+
+
+def test_reused_schedule():
+    """A schedule built once serves every batch of the same layout."""
+    key = synth.key256()
+    buf, off, lens, L = _layout(10_000, 0, 1500, seed=13)
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    d_len = torch.from_numpy(lens.view(np.int32)).cuda()
+    sched = engine.ragged_order(d_off, d_len, len(L), "hh")
+    for seed in (21, 22):
+        b = synth.counter_bytes(seed, len(buf))
+        want = oracle.batch_ragged(oracle.ALG_HIGHWAY, key, b, off, lens, 64, 4)
+        got = engine.highway_ragged(key, torch.from_numpy(b).cuda(), d_off, d_len, 64,
+                                    kernel=KERNEL_RING, schedule=sched)
+        assert np.array_equal(engine.to_u64(got), want)
+    with pytest.raises(ValueError):
+        engine.highway_ragged(key, torch.from_numpy(buf).cuda(), d_off, d_len, 64,
+                              kernel=KERNEL_RING, schedule=sched[:-1])
+    with pytest.raises(ValueError):
+        engine.highway_ragged(key, torch.from_numpy(buf).cuda(), d_off, d_len, 64,
+                              kernel=engine.KERNEL_STAGED, schedule=sched)
